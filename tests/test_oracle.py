@@ -1,0 +1,456 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (-m "not gpu").
+
+Each test names the pin of DESIGN.md §6 it implements.  None of these
+re-types the oracle's own formula: they compare it with published known
+answers, closed forms derived independently (max-plus recursions, M/D/1,
+single-type fluid), the paper's worked examples, invariants, and brute force.
+"""
+import decimal
+import itertools
+import math
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from oracle import F
+from oracle import fluid as fl
+
+TPS = 10 ** 12  # ticks per second (1 tick = 1 ps)
+
+
+# --------------------------------------------------------------- P1 Philox
+def test_philox_known_answers():
+    """Random123 known-answer vectors for Philox4x32-10."""
+    assert oracle.philox([0, 0, 0, 0], [0, 0]) == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    assert oracle.philox([0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2) == [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]
+    assert oracle.philox([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], [0xA4093822, 0x299F31D0]) == \
+        [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]
+
+
+# ------------------------------------------------------------ P2 -ln U
+def _ulps(a, b):
+    return abs(np.float64(a).view(np.int64) - np.float64(b).view(np.int64))
+
+
+def test_neglog_sampler_accuracy():
+    """-ln U within 4 ulp of a 50-digit reference, U = (2 u52 + 1) 2^-53."""
+    decimal.getcontext().prec = 50
+    rng = random.Random(1)
+    cases = [(0, 0), (0xFFFFFFFF, 0xFFFFFFFF), (0x80000000, 0), (0x5A827999, 0x12345678)]
+    cases += [(rng.getrandbits(32), rng.getrandbits(32)) for _ in range(3000)]
+    cases += [(0xFFFFFFFF, rng.getrandbits(32)) for _ in range(200)]  # U -> 1
+    cases += [(0, rng.getrandbits(32)) for _ in range(200)]           # U -> 0
+    worst = 0
+    for x0, x1 in cases:
+        v = 2 * ((x0 << 20) | (x1 >> 12)) + 1
+        ref = -(decimal.Decimal(v) / decimal.Decimal(2 ** 53)).ln()
+        got = oracle.exp_from_bits(x0, x1)
+        worst = max(worst, _ulps(got, float(ref)))
+    assert worst <= 4
+    assert oracle.exp_from_bits(0, 0) == pytest.approx(36.7368005696771, rel=1e-15)
+    assert oracle.exp_from_bits(0xFFFFFFFF, 0xFFFFFFFF) == pytest.approx(1.1102230246251565e-16, rel=1e-14)
+
+
+# ------------------------------------------------------- P3 Poisson streams
+def test_poisson_counts_and_gaps():
+    """Arrival counts in [0,T) are Poisson(lambda T); gaps are Exp(lambda)."""
+    wl = W.Workload("p", [50.0], [W.fixed(1)], [W.fixed(1)], M=100, horizon_s=20.0, seed=7)
+    counts = []
+    for r in range(300):
+        t, _, _ = oracle.gen_arrivals(wl, r, 0, 2000)
+        counts.append(int((t < 20 * TPS).sum()))
+    counts = np.array(counts, dtype=float)
+    mu = 50 * 20
+    assert abs(counts.mean() - mu) < 4 * math.sqrt(mu / len(counts))
+    assert abs(counts.var(ddof=1) / mu - 1) < 0.25
+    t, _, _ = oracle.gen_arrivals(wl, 0, 0, 20000)
+    gaps = np.diff(np.concatenate([[0], t])) / TPS
+    # Kolmogorov-Smirnov against Exp(50)
+    g = np.sort(gaps)
+    cdf = 1 - np.exp(-50 * g)
+    D = np.max(np.abs(cdf - (np.arange(1, len(g) + 1) / len(g))))
+    assert D < 1.63 / math.sqrt(len(g))  # 1% level
+    # classes are independent streams: class 1 differs from class 0
+    wl2 = W.Workload("p2", [50.0, 50.0], [W.fixed(1)] * 2, [W.fixed(1)] * 2, M=100, horizon_s=1, seed=7)
+    a, _, _ = oracle.gen_arrivals(wl2, 0, 0, 100)
+    b, _, _ = oracle.gen_arrivals(wl2, 0, 1, 100)
+    assert not np.array_equal(a, b)
+
+
+# ---------------------------------------------------------- P4 length CDF
+def test_length_tables_match_weights():
+    """Sampled l, l' frequencies match integer weights (chi-square), and a
+    1-entry table is a fixed length."""
+    tab = [(3, 5), (7, 1), (9, 10), (11, 4)]
+    wl = W.Workload("t", [100.0], [tab], [W.fixed(4)], M=100, horizon_s=1, seed=11)
+    n = 200_000
+    _, l, lp = oracle.gen_arrivals(wl, 0, 0, n)
+    assert set(lp.tolist()) == {4}
+    W_ = sum(w for _, w in tab)
+    chi2 = 0.0
+    for v, w in tab:
+        exp = n * w / W_
+        chi2 += (np.sum(l == v) - exp) ** 2 / exp
+    assert chi2 < 16.27  # chi2(3) at 0.1%
+    assert set(l.tolist()) <= {v for v, _ in tab}
+
+
+def test_length_table_extreme_weights():
+    """A weight-0 entry is never drawn; a dominant weight takes almost all."""
+    tab = [(1, 0), (2, 1), (3, 2 ** 40)]
+    wl = W.Workload("t", [100.0], [tab], [W.fixed(1)], M=100, horizon_s=1, seed=3)
+    _, l, _ = oracle.gen_arrivals(wl, 0, 0, 50_000)
+    assert 1 not in set(l.tolist())
+    assert np.mean(l == 3) > 0.999
+
+
+# ------------------------------------------------------------ P5 fluid
+def test_fluid_golden_instance():
+    """Prop. 3 instance (1,1,1),(1,2,1), d0=1/2, d1=1/18: rho=1/2, dT*=1,
+    n*=(2,3), M*=9, Throughput*=3."""
+    f = fl.fluid(W.GOLDEN)
+    assert float(f.rho) == pytest.approx(0.5, rel=1e-12)
+    assert float(f.dT) == pytest.approx(1.0, rel=1e-12)
+    assert [float(x) for x in f.n_star] == pytest.approx([2.0, 3.0], rel=1e-12)
+    assert float(f.M_star) == pytest.approx(9.0, rel=1e-12)
+    assert float(f.thr_star) == pytest.approx(3.0, rel=1e-12)
+
+
+def test_fluid_example2_and_instability():
+    """Example 2 system (l=l'=1, lambda=4, d0=1/2, d1=1/24): 4 per stage, M*=12
+    (PAPER.md:1439); rho >= 1 is unstable (Prop. 1)."""
+    f = fl.fluid(W.EX2)
+    assert float(f.M_star) == pytest.approx(12.0, rel=1e-12)
+    assert [float(x) for x in f.n_star] == pytest.approx([8.0], rel=1e-12)  # 4 per stage x 2 stages
+    hot = W.Workload("hot", [1.0 / (W.D1_S * 17 * 16)], [W.fixed(8)], [W.fixed(16)], M=1000,
+                     horizon_s=1, seed=1)
+    assert not fl.fluid(hot).stable
+
+
+@pytest.mark.parametrize("l,lp,lam", [(8, 16, 74.0), (20, 100, 30.0), (1, 1, 4.0)])
+def test_single_type_closed_form_equals_multi_type(l, lp, lam):
+    """Single-type formulas == multi-type fluid with m=1
+    (PAPER.md:1331-1361); Throughput* = lambda l'."""
+    wl = W.Workload("s", [lam], [W.fixed(l)], [W.fixed(lp)], M=10 ** 6, horizon_s=1, seed=1)
+    n, M, thr = fl.single_type(l, lp, lam, W.D0_S, W.D1_S)
+    f = fl.fluid(wl)
+    assert float(f.n_star[0]) == pytest.approx(float(n), rel=1e-12)
+    assert float(f.M_star) == pytest.approx(float(M), rel=1e-12)
+    assert float(f.thr_star) == pytest.approx(lam * lp, rel=1e-12)
+
+
+def test_fluid_c1_values():
+    n, M, thr = fl.single_type(8, 16, 74.0, W.D0_S, W.D1_S)
+    assert float(n) == pytest.approx(15.2031, abs=5e-4)
+    assert float(M) == pytest.approx(243.250, abs=5e-3)
+    assert float(thr) == pytest.approx(1184.0)
+
+
+# ------------------------------------------------------- P5b thresholds
+def test_threshold_recipes_regression_and_minimality():
+    assert fl.wait_fluid_integer(W.C1) == [1]
+    assert fl.wait_fluid_integer(W.C2) == [16, 16]
+    assert fl.wait_heuristic(W.C2, 1024) == [47, 24]
+    assert [fl.wait_fluid_integer(W.c4(i)) for i in range(5)] == \
+        [[2, 2, 1], [3, 2, 1], [6, 4, 2], [9, 6, 3], [18, 12, 6]]
+    seg3a = [20, 40, 80, 160]
+    assert fl.nested_strict(W.C3A, seg3a) == [7, 7, 7, 5]
+    assert fl.nested_strict(W.C3B, [50 * k for k in range(1, 11)]) == [8, 5, 4, 3, 2, 2, 2, 2, 1, 1]
+    # C3a: n_3 = floor(7 * 12/14) + 1 = 7 needs exact arithmetic (7*12/14 = 6)
+    assert fl.nested_from_n1(W.C3A, seg3a, 7)[2] == 7
+    # feasibility (Eq. wait_thresholds) holds and one less fails
+    n = fl.wait_fluid_integer(W.C2)
+    assert fl.wait_feasible(W.C2, n) and not fl.wait_feasible(W.C2, [15, 15])
+    # strict nested: p-ratio condition of Eq. nested_wait_thresholds
+    tails = fl.nested_tails(W.C3A, seg3a)
+    nn = fl.nested_strict(W.C3A, seg3a)
+    for k in range(3):
+        assert nn[k + 1] * tails[k] > nn[k] * tails[k + 1]
+    assert not fl.nested_dT_ok(W.C3A, seg3a, fl.nested_from_n1(W.C3A, seg3a, 6))
+
+
+def test_nested_memory_exact_vs_paper_formula():
+    """The exact stage sum and the printed formula agree for <= 2 segments
+    and differ beyond (reading R9; C3a values derived by hand)."""
+    seg = [20, 40, 80, 160]
+    assert fl.nested_memory_exact(W.C3A, seg, [7, 7, 7, 5]) == 80550
+    assert fl.nested_memory_exact(W.C3A, seg, [15, 14, 12, 8]) == 135000
+    assert float(fl.nested_memory_paper(W.C3A, seg, [16, 15, 13, 9])) == pytest.approx(175200)
+    assert fl.nested_memory_exact(W.C3A, seg, [16, 15, 13, 9]) == 149490
+    # one segment: exact = sum_{s=0}^{l'} (l+s) * n = WAIT M^pi
+    one = W.Workload("o", [10.0], [W.fixed(8)], [W.fixed(16)], M=10 ** 5, horizon_s=1, seed=1)
+    assert fl.nested_memory_exact(one, [16], [3]) == fl.wait_memory(one, [3])
+
+
+# ------------------------------------------------------------ P18 theta
+@pytest.mark.parametrize("n_prev,n_k,p,expect", [(10, 6, 0.5, 0.822163), (7, 5, 2.0 / 3.0, 0.453629)])
+def test_theta_root(n_prev, n_k, p, expect):
+    th = fl.theta(n_prev, n_k, p)
+    decimal.getcontext().prec = 40
+    D = decimal.Decimal
+    resid = -D(th) * n_k + n_prev * (1 - D(p) + D(p) * D(th).exp()).ln()
+    assert abs(resid) < D("1e-10")
+    assert th >= 8 * (n_k - n_prev * p) / n_prev  # Lemma lower bound
+    assert th == pytest.approx(expect, abs=1e-6)
+    # small-D approximation 2D/(n p (1-p))
+    th_s = fl.theta(1000, 501, 0.5)
+    assert th_s == pytest.approx(2 * 1 / (1000 * 0.25), rel=0.05)
+
+
+def test_thm2_budget_c3a():
+    base, queue, hp, tot = fl.thm2_budget(W.C3A, [20, 40, 80, 160], [7, 7, 7, 5], 1357, 0.1)
+    assert base == 80550 and queue == (10 + 20) * 7 + (10 + 40) * 7 + (10 + 80) * 5
+    assert tot == pytest.approx(83666, abs=1)
+
+
+# -------------------------------------------------- worked examples (DES)
+def _ex2_trace():
+    """Example 2: 3 arrivals at t=0, 6 during batch 1,
+    4 during every later batch (batch lengths from the token counts)."""
+    d0, d1 = TPS // 2, round(TPS / 24)
+    toks = [3, 12, 12, 12, 11, 11, 11]
+    tr = [(0, 0, 1, 1)] * 3
+    t = 0
+    for k, tok in enumerate(toks):
+        tau = d0 + d1 * tok
+        n = 6 if k == 0 else 4
+        tr += [(t + tau * (i + 1) // (n + 1), 0, 1, 1) for i in range(n)]
+        t += tau
+    return tr, t
+
+
+def test_example2_fcfs_cascade():
+    """P11.  First three batches are the paper's: 'memory exactly full with
+    only 3 completions', then 'evict 2 decode prompts ... 4+8 = 12'
+    (PAPER.md:1441-1442).  Batches 4-7 follow from the FCFS rules by hand:
+    b4 FIFO [R,R,a,a,a,a]: KV 4+6<=12 admit 6, peak 4+4+6=14 -> evict 1;
+    b5 [R,a x4]: admit 5, peak 6+6+5=17 -> evict 3; b6 [R,R,R,a x4]: admit 7,
+    peak 5+5+7=17 -> evict 3; b7 [R,R,R,a x4]: 7+5<=12 admits 5, peak
+    7+7+5=19 -> evict 4."""
+    tr, t_end = _ex2_trace()
+    rows, log = oracle.run_trace(W.EX2, W.Policy(W.FCFS, B=1000), [0], [tr], log_cap=16,
+                                 horizon_s=t_end / TPS)
+    got = [(int(r[2]), int(r[3]), int(r[4]), int(r[5])) for r in log]
+    assert got[:3] == [(3, 0, 0, 3), (12, 3, 0, 6), (12, 4, 2, 4)]
+    assert got[3:7] == [(12, 3, 1, 6), (11, 3, 3, 5), (11, 2, 3, 7), (11, 3, 4, 5)]
+    assert all(int(r[6]) <= 12 for r in log)   # peak never exceeds C
+    # Example 1: 4 prefill + 4 decode = 4 + 8 = 12 units
+    assert got[2][0] == 4 * 1 + 4 * 2
+
+
+# ----------------------------------------------- closed-form trajectories
+def _wait_maxplus(a, n, l, lp, d0, d1, T):
+    """Single-type WAIT without eviction as a max-plus (G/D/1 Lindley)
+    recursion [derived]: batch b starts at max(E_{b-1}, a_{bn}), carries
+    cohorts b, b-1, .., b-l' at stages 0..l', and cohort b completes at
+    E_{b+l'} and emits its first token at E_{b+1}."""
+    a = [x for x in a if x < T]
+    E, S = [0], []
+    b = 1
+    while b * n <= len(a):
+        s = max(E[-1], a[b * n - 1])
+        if s >= T:
+            break
+        tok = n * sum(l + j for j in range(min(b - 1, lp) + 1))
+        S.append(s)
+        E.append(s + d0 + d1 * tok)
+        b += 1
+    nb = len(S)
+    done = lat = ttft = nft = after = 0
+    for c in range(1, nb + 1):
+        coh = a[(c - 1) * n: c * n]
+        if c + 1 <= nb and E[c + 1] <= T:
+            ttft += sum(E[c + 1] - x for x in coh)
+            nft += n
+        if c + lp <= nb:
+            if E[c + lp] <= T:
+                done += n
+                lat += sum(E[c + lp] - x for x in coh)
+            else:
+                after += n
+    return dict(batches=nb, completed=done, lat=lat, ttft=ttft, first_tokens=nft,
+                completed_after_T=after, busy=sum(E[i + 1] - S[i] for i in range(nb)))
+
+
+def _check_maxplus(wl, n, seed_rep=0):
+    l, lp = wl.l_tab[0][0][0], wl.lp_tab[0][0][0]
+    d0, d1, T = round(wl.d0_s * TPS), round(wl.d1_s * TPS), round(wl.horizon_s * TPS)
+    t, _, _ = oracle.gen_arrivals(wl, seed_rep, 0, int(wl.lam[0] * wl.horizon_s * 2 + 100))
+    ref = _wait_maxplus(t.tolist(), n, l, lp, d0, d1, T)
+    rows = oracle.run(wl, W.Policy(W.WAIT), [n], n_reps=1, rep_begin=seed_rep)
+    assert rows[F["evictions"], 0] == 0
+    for k in ["batches", "completed", "first_tokens", "completed_after_T"]:
+        assert int(rows[F[k], 0]) == ref[k], k
+    assert oracle.u128(rows, "lat")[0] == ref["lat"]
+    assert oracle.u128(rows, "ttft")[0] == ref["ttft"]
+    assert int(rows[F["busy_ticks"], 0]) == ref["busy"]
+
+
+def test_wait_single_type_maxplus_c1p():
+    """P7 on C1' (M = M^pi = 272, n = 1)."""
+    _check_maxplus(W.C1P, 1)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_wait_single_type_maxplus_random(seed):
+    rng = random.Random(seed)
+    l, lp, n = rng.randint(1, 9), rng.randint(1, 12), rng.randint(1, 4)
+    Mpi = n * sum(l + s for s in range(lp + 1))
+    wl = W.Workload("mp", [rng.choice([20.0, 80.0, 300.0])], [W.fixed(l)], [W.fixed(lp)],
+                    M=Mpi + rng.randint(0, 3), horizon_s=rng.choice([1.0, 3.0]), seed=seed + 100,
+                    d0_s=rng.choice([0.002, 0.01]), d1_s=rng.choice([1e-5, 2e-4]))
+    _check_maxplus(wl, n, seed_rep=seed)
+
+
+def test_fcfs_b1_is_md1():
+    """P9: FCFS with B=1 and ample memory serves one prompt at a time through
+    its l'+1 iterations: E_i = max(E_{i-1}, a_i) + sum_s (d0 + d1 (l+s))."""
+    wl = W.Workload("md1", [30.0], [W.fixed(5)], [W.fixed(4)], M=10 ** 6, horizon_s=20.0, seed=5)
+    d0, d1, T = round(wl.d0_s * TPS), round(wl.d1_s * TPS), round(wl.horizon_s * TPS)
+    t, _, _ = oracle.gen_arrivals(wl, 0, 0, 2000)
+    a = [x for x in t.tolist() if x < T]
+    E, done, lat, ttft, nft, batches = 0, 0, 0, 0, 0, 0
+    for x in a:
+        s = max(E, x)
+        ends = []
+        for st in range(5):
+            if s >= T:
+                break
+            s += d0 + d1 * (5 + st)
+            ends.append(s)
+            batches += 1
+        if len(ends) >= 2 and ends[1] <= T:
+            ttft += ends[1] - x
+            nft += 1
+        if len(ends) == 5:
+            E = ends[-1]
+            if E <= T:
+                done += 1
+                lat += E - x
+        else:
+            break
+    rows = oracle.run(wl, W.Policy(W.FCFS, B=1), [0])
+    assert int(rows[F["completed"], 0]) == done
+    assert int(rows[F["batches"], 0]) == batches
+    assert oracle.u128(rows, "lat")[0] == lat
+    assert oracle.u128(rows, "ttft")[0] == ttft
+    assert int(rows[F["first_tokens"], 0]) == nft
+
+
+def test_nested_one_segment_equals_wait():
+    """P10: Nested WAIT with a single segment is WAIT with one type."""
+    for wl, n in [(W.C1, 1), (W.C1P, 1), (W.C1, 2)]:
+        a = oracle.run(wl, W.Policy(W.WAIT), [n], n_reps=3)
+        b = oracle.run(wl, W.Policy(W.NESTED, seg_end=[16]), [n], n_reps=3)
+        assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------ invariants
+def _invariants(rows, wl, T_t):
+    f = lambda k: rows[F[k]].astype(object)
+    n = rows.shape[1]
+    assert (f("arrivals") == f("completed") + f("completed_after_T") + f("final_waiting")
+            + f("final_resident")).all()                       # P13 conservation
+    assert (rows[F["max_kv_peak"]] <= wl.M).all()               # P12 memory
+    assert (f("busy_ticks") + f("idle_ticks") == f("now_stop")).all()
+    assert (f("prefill_steps") == f("admitted")).all()
+    assert (f("admitted") <= f("arrivals") + f("evictions")).all()
+    assert (rows[F["status"]] == 0).all()
+    assert (f("completed_tokens") >= f("completed")).all()
+    assert (f("first_tokens") >= f("completed")).all()
+
+
+@pytest.mark.parametrize("seed", range(25))
+def test_random_workload_invariants(seed):
+    rng = np.random.default_rng(seed)
+    wl = W.random_small(rng)
+    T_t = round(wl.horizon_s * TPS)
+    maxlp = max(v for t in wl.lp_tab for v, _ in t)
+    pols = [(W.Policy(W.WAIT), [int(rng.integers(1, 4)) for _ in range(wl.K)]),
+            (W.Policy(W.FCFS, B=int(rng.integers(1, 20))), [0]),
+            (W.Policy(W.NESTED, seg_end=sorted({int(x) for x in rng.integers(1, maxlp, 2)} | {maxlp})), None)]
+    for pol, thr in pols:
+        if thr is None:
+            thr = sorted([int(x) for x in rng.integers(1, 4, len(pol.seg_end))], reverse=True)
+        rows = oracle.run(wl, pol, thr, n_reps=4)
+        _invariants(rows, wl, T_t)
+        again = oracle.run(wl, pol, thr, n_reps=4)
+        assert np.array_equal(rows, again)                      # P21 determinism
+        # sharding invariance: replication rows depend on the global index only
+        part = oracle.run(wl, pol, thr, n_reps=2, rep_begin=2)
+        assert np.array_equal(rows[:, 2:], part)
+
+
+def test_wait_no_eviction_when_memory_covers_mpi():
+    """P12: WAIT with M >= M^pi never evicts and peaks at most M^pi
+    (PAPER.md:1521); C2 is such a case."""
+    n = [16, 16]
+    rows = oracle.run(W.C2, W.Policy(W.WAIT), n, n_reps=2, horizon_s=2.0)
+    assert (rows[F["evictions"]] == 0).all()
+    assert (rows[F["max_kv_peak"]] <= fl.wait_memory(W.C2, n)).all()
+
+
+# ------------------------------------------------------- brute force P20
+def test_bruteforce_tiny_traces():
+    """Every multiset of <= 5 arrivals on a 5-point grid: invariants for the
+    three policies, and single-type WAIT == max-plus when M >= M^pi."""
+    unit = 4 * 10 ** 9  # 4 ms grid
+    cnt = 0
+    for l, lp in [(1, 1), (1, 2), (2, 1), (2, 2)]:
+        wl = W.Workload("bf", [1.0], [W.fixed(l)], [W.fixed(lp)], M=8, horizon_s=0.1,
+                        seed=0, d0_s=0.005, d1_s=0.001)
+        T = round(wl.horizon_s * TPS)
+        traces = []
+        for k in range(6):
+            for combo in itertools.combinations_with_replacement(range(5), k):
+                traces.append([(x * unit, 0, l, lp) for x in combo])
+        for M in range(l + lp, 9):
+            wlm = W.Workload("bf", [1.0], [W.fixed(l)], [W.fixed(lp)], M=M, horizon_s=0.1,
+                             seed=0, d0_s=0.005, d1_s=0.001)
+            for pol, thr in [(W.Policy(W.FCFS, B=3), [0]), (W.Policy(W.WAIT), [1]),
+                             (W.Policy(W.WAIT), [2]), (W.Policy(W.NESTED, seg_end=[lp]), [2])]:
+                rows, _ = oracle.run_trace(wlm, pol, thr, traces)
+                _invariants(rows, wlm, T)
+                n = thr[0]
+                if pol.kind == W.WAIT and M >= n * sum(l + s for s in range(lp + 1)):
+                    for i, tr in enumerate(traces):
+                        ref = _wait_maxplus([x[0] for x in tr], n, l, lp, 5 * 10 ** 9, 10 ** 9, T)
+                        assert int(rows[F["batches"], i]) == ref["batches"]
+                        assert int(rows[F["completed"], i]) == ref["completed"]
+                        assert int(rows[F["lat_lo"], i]) == ref["lat"]
+                        cnt += 1
+    assert cnt > 1000
+
+
+# ------------------------------------------------------ statistical pins
+def test_md1_steady_state_c1p():
+    """P8: single-type WAIT with n=1 is an M/D/1 queue for batch starts
+    (Pollaczek-Khinchine): E[latency] = W_q + dT + l'/lambda,
+    E[TTFT] = W_q + dT + 1/lambda with dT = d0 + d1 M^pi."""
+    lam, dT = 74.0, W.D0_S + W.D1_S * 272
+    Wq = lam * dT ** 2 / (2 * (1 - lam * dT))
+    rows = oracle.run(W.C1P, W.Policy(W.WAIT), [1], n_reps=400, n_threads=8,
+                      horizon_s=5 * 2000 / 74)
+    lat = np.array(oracle.u128(rows, "lat"), float) / rows[F["completed"]] / TPS
+    tt = np.array(oracle.u128(rows, "ttft"), float) / rows[F["first_tokens"]] / TPS
+    se_l, se_t = lat.std(ddof=1) / math.sqrt(len(lat)), tt.std(ddof=1) / math.sqrt(len(tt))
+    assert abs(lat.mean() - (Wq + dT + 16 / lam)) < 3 * se_l + 5e-4
+    assert abs(tt.mean() - (Wq + dT + 1 / lam)) < 3 * se_t + 5e-4
+
+
+def test_littles_law_and_prop2_c2():
+    """P15 Little's law L = lambda W on a long C2 run, and P16 Prop. 2:
+    throughput <= Throughput* when C >= M* (PAPER.md:1364-1370)."""
+    for pol, thr in [(W.Policy(W.WAIT), [16, 16]), (W.Policy(W.FCFS, B=1024), [0])]:
+        rows = oracle.run(W.C2, pol, thr, n_reps=8, n_threads=8, horizon_s=100.0)
+        T = 100.0
+        L = np.array(oracle.u128(rows, "soj"), float) / TPS / T
+        lat = np.array(oracle.u128(rows, "lat"), float) / TPS / rows[F["completed"]]
+        lamW = rows[F["arrivals"]] / T * lat
+        assert np.all(np.abs(L / lamW - 1) < 0.01)
+        thr_tok = rows[F["completed_tokens"]] / T
+        se = thr_tok.std(ddof=1) / math.sqrt(len(thr_tok))
+        assert thr_tok.mean() <= float(fl.fluid(W.C2).thr_star) + 3 * se
