@@ -349,6 +349,8 @@ struct Sim {
       bool go = decide(P);                        // step 3
       uint64_t n_evict = 0;
       int64_t peak = 0;
+      uint64_t waiting = 0;  // waiting prompts at decision time (before admission/eviction)
+      for (auto& q : fifo) waiting += q.size();
       if (go) {
         // step 4, MEMORY: the KV held after this iteration must fit in M
         // (Eq. memory_constraint; paused prompts keep their
@@ -390,8 +392,6 @@ struct Sim {
       }
       // step 5, EXECUTE.  tau = d0 + d1 * (sum_prefill l + sum_decode (l+s))
       // (Eq. time_consump).
-      uint64_t waiting = 0;
-      for (auto& q : fifo) waiting += q.size();
       sum_waiting += waiting;
       int64_t tokens = 0;
       uint64_t n_res_plan = 0;

@@ -1,0 +1,473 @@
+// sched_api.cpp -- the C ABI of libsched (include/sched.h): config
+// validation and upload, launch sizing, sched_run / sched_run_host /
+// sched_run_trace.  All simulation work runs in sim_kernel.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sched.h"
+#include "setup.h"
+#include "sim_internal.h"
+
+using namespace waitsim;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(SCHED_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x)                                      \
+  do {                                             \
+    cudaError_t e_ = (x);                          \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #x); \
+  } while (0)
+}  // namespace
+
+struct sched_s {
+  SetupInput in;
+  uint32_t tok_budget = 0, max_resident_cfg = 0, ring_cap = 8192;
+  int device = 0;
+  int64_t d0_t = 0, d1_t = 0;
+  uint32_t max_lp = 0, min_l = 0;
+  DevParams base{};
+  // device-side tables
+  uint64_t* d_cdf_thr = nullptr;
+  uint16_t* d_cdf_val = nullptr;
+  uint8_t* d_stage_info = nullptr;
+  std::vector<uint64_t> h_cdf_thr;     // uploaded lazily by prepare()
+  std::vector<uint16_t> h_cdf_val;
+  std::vector<uint8_t> h_stage_info;
+  // scratch
+  int64_t* d_ring_a = nullptr;
+  int64_t* d_ring_e = nullptr;
+  uint32_t* d_ring_llp = nullptr;
+  size_t ring_entries = 0;
+  uint32_t* d_counter = nullptr;
+  uint64_t* d_out = nullptr;
+  size_t out_cap = 0;
+  // launch
+  int grid = 0, block = 0, wpb = 0, blocks_per_sm = 0, sm_count = 0;
+  uint32_t Rc = 0, warp_smem = 0;
+  bool prepared = false;
+};
+
+namespace {
+
+// Resident capacity: FCFS holds at most B prompts; WAIT at most n_j per stage
+// (invariant P14) plus one staged batch; NESTED: non-entry stages hold at
+// most n_k, entry-stage queues are bounded by memory -- take a margin.
+uint32_t derive_rc(const sched_s* h) {
+  if (h->max_resident_cfg) return h->max_resident_cfg;
+  uint64_t rc = 0;
+  const auto& in = h->in;
+  if (in.policy == SCHED_FCFS) {
+    rc = in.B;
+  } else if (in.policy == SCHED_WAIT) {
+    for (size_t c = 0; c < in.thresholds.size(); ++c) {
+      uint32_t mx = 0;
+      for (auto& e : in.lp[c]) mx = std::max<uint32_t>(mx, e.first);
+      rc += (uint64_t)in.thresholds[c] * (mx + 1);
+    }
+  } else {
+    uint64_t prev = 0, base = 0;
+    for (size_t k = 0; k < in.seg_end.size(); ++k) {
+      base += (uint64_t)in.thresholds[k] * (in.seg_end[k] - prev);
+      prev = in.seg_end[k];
+    }
+    rc = base + std::max<uint64_t>(256, base / 2) + in.thresholds[0];
+    rc = std::min<uint64_t>(rc, (uint64_t)in.M / std::max<uint32_t>(1, h->min_l) + in.thresholds[0]);
+  }
+  rc = std::max<uint64_t>(rc, 32);
+  rc = (rc + 31) & ~31ull;
+  // default cap 4096 (64 KiB of shared memory per warp); larger needs an
+  // explicit max_resident.  Overflow is reported per replication (status 1).
+  return (uint32_t)std::min<uint64_t>(rc, 4096);
+}
+
+int prepare(sched_s* h) {
+  if (h->prepared) return 0;
+  if (h->in.policy != SCHED_FCFS && h->in.thresholds.empty())
+    return fail(SCHED_E_INVALID, "thresholds not set: pass them in sched_config or call sched_thresholds");
+  CK(cudaSetDevice(h->device));
+  if (!h->d_cdf_thr) {
+    CK(cudaMalloc(&h->d_cdf_thr, h->h_cdf_thr.size() * 8));
+    CK(cudaMalloc(&h->d_cdf_val, h->h_cdf_val.size() * 2));
+    CK(cudaMemcpy(h->d_cdf_thr, h->h_cdf_thr.data(), h->h_cdf_thr.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->d_cdf_val, h->h_cdf_val.data(), h->h_cdf_val.size() * 2, cudaMemcpyHostToDevice));
+    if (!h->h_stage_info.empty()) {
+      CK(cudaMalloc(&h->d_stage_info, h->h_stage_info.size()));
+      CK(cudaMemcpy(h->d_stage_info, h->h_stage_info.data(), h->h_stage_info.size(), cudaMemcpyHostToDevice));
+    }
+    h->base.cdf_thr = h->d_cdf_thr;
+    h->base.cdf_val = h->d_cdf_val;
+    h->base.stage_info = h->d_stage_info;
+  }
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, h->device));
+  h->sm_count = prop.multiProcessorCount;
+  h->Rc = derive_rc(h);
+  const int K = (int)h->in.lambda.size();
+  h->warp_smem = warp_smem_bytes(h->Rc, K);
+  // choose warps per block maximising resident warps per SM
+  int best_w = 0, best_wpb = 1, best_bps = 0;
+  const int cands[] = {8, 4, 2, 1};
+  for (int wpb : cands) {
+    const size_t smem = (size_t)wpb * h->warp_smem;
+    if (smem > (size_t)prop.sharedMemPerBlockOptin) continue;
+    // max blocks per SM from shared memory and registers (occupancy API)
+    int bps = 0;
+    const cudaError_t e = sim_occupancy(h->in.policy, 0, wpb * 32, smem, &bps);
+    if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+    if (bps * wpb > best_w) { best_w = bps * wpb; best_wpb = wpb; best_bps = bps; }
+  }
+  if (best_w == 0)
+    return fail(SCHED_E_INVALID, "resident capacity too large for shared memory (max_resident=" +
+                                     std::to_string(h->Rc) + ")");
+  h->wpb = best_wpb;
+  h->blocks_per_sm = best_bps;
+  h->block = best_wpb * 32;
+  h->grid = h->sm_count * best_bps;
+  const int n_rings = h->in.policy == SCHED_WAIT ? K : 1;
+  const size_t need = (size_t)h->grid * h->wpb * n_rings * h->ring_cap;
+  if (need > h->ring_entries) {
+    cudaFree(h->d_ring_a); cudaFree(h->d_ring_e); cudaFree(h->d_ring_llp);
+    h->d_ring_a = h->d_ring_e = nullptr; h->d_ring_llp = nullptr;
+    CK(cudaMalloc(&h->d_ring_a, need * 8));
+    CK(cudaMalloc(&h->d_ring_e, need * 8));
+    CK(cudaMalloc(&h->d_ring_llp, need * 4));
+    h->ring_entries = need;
+  }
+  if (!h->d_counter) CK(cudaMalloc(&h->d_counter, 4));
+  DevParams& p = h->base;
+  p.n_rings = n_rings;
+  p.Rc = h->Rc;
+  p.ring_cap = h->ring_cap;
+  p.warp_smem = h->warp_smem;
+  for (size_t i = 0; i < h->in.thresholds.size() && i < 32; ++i) p.thr[i] = h->in.thresholds[i];
+  p.ring_a = h->d_ring_a;
+  p.ring_e = h->d_ring_e;
+  p.ring_llp = h->d_ring_llp;
+  p.work_counter = h->d_counter;
+  h->prepared = true;
+  return 0;
+}
+
+int launch(sched_s* h, DevParams p, cudaStream_t st) {
+  CK(cudaMemsetAsync(h->d_counter, 0, 4, st));
+  const size_t smem = (size_t)h->wpb * h->warp_smem;
+  int grid = h->grid;
+  const int warps = grid * h->wpb;
+  if ((int64_t)p.n_reps < warps) grid = std::max<int>(1, (int)((p.n_reps + h->wpb - 1) / h->wpb));
+  CK(launch_sim(p, grid, h->block, smem, st));
+  return 0;
+}
+
+bool table_ok(const uint32_t* off, const uint64_t* w, uint32_t c) {
+  if (off[c + 1] <= off[c]) return false;
+  uint64_t tot = 0;
+  for (uint32_t i = off[c]; i < off[c + 1]; ++i) tot |= w[i];
+  return tot != 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sched_last_error(void) { return g_err.c_str(); }
+
+int sched_create(sched_t* out, const sched_config* cfg) {
+  if (!out || !cfg) return fail(SCHED_E_INVALID, "null argument");
+  *out = nullptr;
+  const uint32_t K = cfg->K;
+  if (K == 0 || K > 32) return fail(SCHED_E_INVALID, "K must be 1..32");
+  if (!cfg->lambda || !cfg->l_off || !cfg->l_val || !cfg->l_w || !cfg->lp_off || !cfg->lp_val ||
+      !cfg->lp_w)
+    return fail(SCHED_E_INVALID, "null table pointer");
+  if (!(cfg->d0_s > 0) || !(cfg->d1_s >= 0)) return fail(SCHED_E_INVALID, "need d0 > 0, d1 >= 0");
+  if (cfg->M < 1) return fail(SCHED_E_INVALID, "M must be >= 1");
+  if (cfg->policy < SCHED_WAIT || cfg->policy > SCHED_FCFS) return fail(SCHED_E_INVALID, "bad policy");
+  sched_s* h = new sched_s();
+  SetupInput& in = h->in;
+  in.d0_s = cfg->d0_s; in.d1_s = cfg->d1_s; in.M = cfg->M; in.policy = cfg->policy; in.B = cfg->B;
+  uint32_t max_lp = 0, min_l = 0xFFFF, max_l = 0;
+  std::vector<uint64_t> thr_all;
+  std::vector<uint16_t> val_all;
+  for (uint32_t c = 0; c < K; ++c) {
+    if (!(cfg->lambda[c] >= 0) || std::isinf(cfg->lambda[c])) { delete h; return fail(SCHED_E_INVALID, "lambda must be finite and >= 0"); }
+    if (!table_ok(cfg->l_off, cfg->l_w, c) || !table_ok(cfg->lp_off, cfg->lp_w, c)) {
+      delete h;
+      return fail(SCHED_E_INVALID, "empty or zero-weight length table");
+    }
+    in.lambda.push_back(cfg->lambda[c]);
+    Table lt, lpt;
+    uint32_t cmax_l = 0, cmax_lp = 0;
+    for (uint32_t i = cfg->l_off[c]; i < cfg->l_off[c + 1]; ++i) {
+      if (cfg->l_val[i] < 1) { delete h; return fail(SCHED_E_INVALID, "prefill length must be >= 1"); }
+      lt.push_back({cfg->l_val[i], cfg->l_w[i]});
+      if (cfg->l_w[i]) { cmax_l = std::max<uint32_t>(cmax_l, cfg->l_val[i]); min_l = std::min<uint32_t>(min_l, cfg->l_val[i]); }
+    }
+    for (uint32_t i = cfg->lp_off[c]; i < cfg->lp_off[c + 1]; ++i) {
+      if (cfg->lp_val[i] < 1 || cfg->lp_val[i] > 32767) { delete h; return fail(SCHED_E_INVALID, "decode length must be 1..32767"); }
+      lpt.push_back({cfg->lp_val[i], cfg->lp_w[i]});
+      if (cfg->lp_w[i]) cmax_lp = std::max<uint32_t>(cmax_lp, cfg->lp_val[i]);
+    }
+    if (cfg->lambda[c] > 0 && (int64_t)cmax_l + cmax_lp > cfg->M) {
+      delete h;
+      return fail(SCHED_E_UNSATISFIABLE, "some l + l' exceeds M: that prompt can never complete");
+    }
+    max_lp = std::max(max_lp, cmax_lp);
+    max_l = std::max(max_l, cmax_l);
+    in.l.push_back(lt);
+    in.lp.push_back(lpt);
+    // integer CDF tables: thr_i = floor(cum_i 2^32 / W)
+    for (int which = 0; which < 2; ++which) {
+      const Table& t = which ? lpt : lt;
+      unsigned __int128 W = 0, cum = 0;
+      for (auto& e : t) W += e.second;
+      ClassParam& cp = h->base.cls[c];
+      (which ? cp.lp_off : cp.l_off) = (uint32_t)thr_all.size();
+      (which ? cp.lp_n : cp.l_n) = (uint32_t)t.size();
+      for (size_t i = 0; i < t.size(); ++i) {
+        cum += t[i].second;
+        uint64_t th = (uint64_t)((cum << 32) / W);
+        if (i + 1 == t.size()) th = (uint64_t)1 << 32;
+        thr_all.push_back(th);
+        val_all.push_back(t[i].first);
+      }
+    }
+    h->base.cls[c].gap_scale = cfg->lambda[c] > 0 ? 1e12 / cfg->lambda[c] : 0.0;
+  }
+  h->max_lp = max_lp;
+  h->min_l = min_l;
+  if (cfg->policy == SCHED_FCFS) {
+    if (cfg->B < 1) { delete h; return fail(SCHED_E_INVALID, "FCFS needs B >= 1"); }
+    if (cfg->tok_budget && cfg->tok_budget < max_l) { delete h; return fail(SCHED_E_INVALID, "tok_budget below the largest prefill length"); }
+  }
+  if (cfg->policy == SCHED_NESTED) {
+    if (cfg->n_seg < 1 || cfg->n_seg > 32 || !cfg->seg_end) { delete h; return fail(SCHED_E_INVALID, "NESTED needs 1..32 segments"); }
+    for (uint32_t k = 0; k < cfg->n_seg; ++k) {
+      if ((k == 0 && cfg->seg_end[0] < 1) || (k > 0 && cfg->seg_end[k] <= cfg->seg_end[k - 1])) {
+        delete h;
+        return fail(SCHED_E_INVALID, "seg_end must be increasing and >= 1");
+      }
+      in.seg_end.push_back(cfg->seg_end[k]);
+    }
+    if (in.seg_end.back() < max_lp) { delete h; return fail(SCHED_E_INVALID, "last segment must reach max l'"); }
+  }
+  const uint32_t want_thr = cfg->policy == SCHED_WAIT ? K : cfg->policy == SCHED_NESTED ? cfg->n_seg : 0;
+  if (cfg->n_thr && cfg->policy != SCHED_FCFS) {
+    if (cfg->n_thr != want_thr || !cfg->thresholds) { delete h; return fail(SCHED_E_INVALID, "threshold count mismatch"); }
+    for (uint32_t i = 0; i < cfg->n_thr; ++i) {
+      if (cfg->thresholds[i] < 1) { delete h; return fail(SCHED_E_INVALID, "thresholds must be >= 1"); }
+      in.thresholds.push_back(cfg->thresholds[i]);
+    }
+  }
+  h->tok_budget = cfg->tok_budget;
+  h->max_resident_cfg = cfg->max_resident;
+  if (cfg->restart_cap) h->ring_cap = cfg->restart_cap;
+  h->device = cfg->device;
+  // ticks
+  h->d0_t = std::llround(cfg->d0_s * 1e12);
+  h->d1_t = std::llround(cfg->d1_s * 1e12);
+  DevParams& p = h->base;
+  p.K = (int32_t)K;
+  p.policy = cfg->policy;
+  p.n_seg = (int32_t)in.seg_end.size();
+  p.d0_t = h->d0_t;
+  p.d1_t = h->d1_t;
+  p.M = cfg->M;
+  p.B = cfg->B;
+  p.tok_budget = cfg->tok_budget;
+  h->h_cdf_thr = std::move(thr_all);
+  h->h_cdf_val = std::move(val_all);
+  if (cfg->policy == SCHED_NESTED) {
+    // stage -> segment index | entry-stage flag << 7 (reading R8)
+    std::vector<uint8_t> info(in.seg_end.back() + 2, 0);
+    for (uint32_t s = 0; s < info.size(); ++s) {
+      uint32_t k = 0;
+      while (k < in.seg_end.size() && s > in.seg_end[k]) ++k;
+      if (k >= in.seg_end.size()) k = 0x7F;
+      const bool entry = k >= 1 && k < in.seg_end.size() && s == (uint32_t)in.seg_end[k - 1] + 1;
+      info[s] = (uint8_t)(k | (entry ? 0x80 : 0));
+    }
+    h->h_stage_info = std::move(info);
+  }
+  *out = h;
+  return SCHED_OK;
+}
+
+int sched_thresholds(sched_t h, int32_t mode, double delta, double budget_B,
+                     sched_threshold_report* out) {
+  if (!h || !out) return fail(SCHED_E_INVALID, "null argument");
+  if (mode < 0 || mode > 1) return fail(SCHED_E_INVALID, "mode must be 0 or 1");
+  std::vector<uint32_t> chosen;
+  std::string err;
+  int rc;
+  try {
+    rc = compute_thresholds(h->in, mode, delta, budget_B, out, &chosen, &err);
+  } catch (const std::exception& ex) {
+    return fail(SCHED_E_INVALID, ex.what());
+  }
+  if (rc == -2 && chosen.empty() && h->in.policy != SCHED_FCFS && h->in.thresholds.empty())
+    return fail(SCHED_E_UNSTABLE, err.empty() ? "rho >= 1" : err);
+  if (rc == -3) return fail(SCHED_E_INFEASIBLE, err);
+  if (rc == -1) return fail(SCHED_E_INVALID, err);
+  if (h->in.thresholds.empty() && !chosen.empty()) {
+    h->in.thresholds = chosen;
+    h->prepared = false;
+  }
+  if (rc == -2) return fail(SCHED_E_UNSTABLE, "rho >= 1 (Prop. 1, PAPER.md:1290)");
+  return SCHED_OK;
+}
+
+int sched_run(sched_t h, uint64_t seed, uint64_t rep_begin, uint32_t n_reps, double horizon_s,
+              uint64_t* out_dev, void* cuda_stream) {
+  if (!h || !out_dev) return fail(SCHED_E_INVALID, "null argument");
+  if (n_reps == 0) return fail(SCHED_E_INVALID, "n_reps must be > 0");
+  if (!(horizon_s > 0) || horizon_s > 1.4e5) return fail(SCHED_E_INVALID, "horizon must be in (0, 1.4e5] s");
+  if (rep_begin + n_reps > (1ull << 32)) return fail(SCHED_E_INVALID, "replication index exceeds 2^32");
+  if (int rc = prepare(h)) return rc;
+  CK(cudaSetDevice(h->device));
+  DevParams p = h->base;
+  p.seed = seed;
+  p.rep_begin = rep_begin;
+  p.n_reps = n_reps;
+  p.T_t = std::llround(horizon_s * 1e12);
+  p.trace_mode = 0;
+  p.out = out_dev;
+  return launch(h, p, (cudaStream_t)cuda_stream);
+}
+
+int sched_run_host(sched_t h, uint64_t seed, uint64_t rep_begin, uint32_t n_reps,
+                   double horizon_s, uint64_t* out_host, void* cuda_stream) {
+  if (!h || !out_host) return fail(SCHED_E_INVALID, "null argument");
+  const size_t bytes = (size_t)SCHED_NF * n_reps * 8;
+  CK(cudaSetDevice(h->device));
+  if (bytes > h->out_cap) {
+    cudaFree(h->d_out);
+    h->d_out = nullptr;
+    CK(cudaMalloc(&h->d_out, bytes));
+    h->out_cap = bytes;
+  }
+  if (int rc = sched_run(h, seed, rep_begin, n_reps, horizon_s, h->d_out, cuda_stream)) return rc;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  CK(cudaMemcpyAsync(out_host, h->d_out, bytes, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return SCHED_OK;
+}
+
+int sched_run_trace(sched_t h, const int64_t* t_ticks, const int32_t* cls, const int32_t* l,
+                    const int32_t* lp, const int64_t* off, uint32_t n_reps, double horizon_s,
+                    uint64_t* out_host, int64_t* log_host, int64_t log_cap, int64_t* n_logged) {
+  if (!h || !off || !out_host || n_reps == 0) return fail(SCHED_E_INVALID, "bad argument");
+  if (!(horizon_s > 0)) return fail(SCHED_E_INVALID, "horizon must be > 0");
+  if (int rc = prepare(h)) return rc;
+  const uint32_t K = (uint32_t)h->in.lambda.size();
+  // regroup every replication's trace by class: slices [tr_off[r*K+c], tr_off[r*K+c+1])
+  std::vector<int64_t> tt, troff;
+  std::vector<uint16_t> tl, tlp;
+  troff.push_back(0);
+  for (uint32_t r = 0; r < n_reps; ++r) {
+    for (uint32_t c = 0; c < K; ++c) {
+      for (int64_t i = off[r]; i < off[r + 1]; ++i) {
+        if (cls[i] < 0 || (uint32_t)cls[i] >= K) return fail(SCHED_E_INVALID, "trace class out of range");
+        if ((uint32_t)cls[i] != c) continue;
+        if (l[i] < 1 || lp[i] < 1 || lp[i] > 32767 || l[i] > 65535) return fail(SCHED_E_INVALID, "bad trace lengths");
+        if (h->in.policy == SCHED_NESTED && lp[i] > (int32_t)h->in.seg_end.back()) return fail(SCHED_E_INVALID, "trace l' beyond the last segment");
+        if ((int64_t)l[i] + lp[i] > h->in.M) return fail(SCHED_E_UNSATISFIABLE, "trace prompt with l + l' > M");
+        if (!tt.empty() && troff.back() < (int64_t)tt.size() && t_ticks[i] < tt.back()) return fail(SCHED_E_INVALID, "trace not sorted by time");
+        tt.push_back(t_ticks[i]);
+        tl.push_back((uint16_t)l[i]);
+        tlp.push_back((uint16_t)lp[i]);
+      }
+      troff.push_back((int64_t)tt.size());
+    }
+  }
+  if (tt.empty()) { tt.push_back(0); tl.push_back(1); tlp.push_back(1); }
+  CK(cudaSetDevice(h->device));
+  int64_t *d_t = nullptr, *d_off = nullptr, *d_log = nullptr, *d_logn = nullptr;
+  uint16_t *d_l = nullptr, *d_lp = nullptr;
+  uint64_t* d_out = nullptr;
+  const size_t out_bytes = (size_t)SCHED_NF * n_reps * 8;
+  int rc = 0;
+  cudaError_t e = cudaMalloc(&d_t, tt.size() * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&d_l, tl.size() * 2);
+  if (e == cudaSuccess) e = cudaMalloc(&d_lp, tlp.size() * 2);
+  if (e == cudaSuccess) e = cudaMalloc(&d_off, troff.size() * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&d_out, out_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&d_log, std::max<int64_t>(1, log_cap) * 7 * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&d_logn, 8);
+  if (e == cudaSuccess) e = cudaMemcpy(d_t, tt.data(), tt.size() * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d_l, tl.data(), tl.size() * 2, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d_lp, tlp.data(), tlp.size() * 2, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d_off, troff.data(), troff.size() * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(d_logn, 0, 8);
+  if (e == cudaSuccess) {
+    DevParams p = h->base;
+    p.seed = 0;
+    p.rep_begin = 0;
+    p.n_reps = n_reps;
+    p.T_t = std::llround(horizon_s * 1e12);
+    p.trace_mode = 1;
+    p.tr_t = d_t; p.tr_l = d_l; p.tr_lp = d_lp; p.tr_off = d_off;
+    p.out = d_out;
+    p.log = d_log;
+    p.log_cap = log_host ? log_cap : 0;
+    p.log_n = d_logn;
+    rc = launch(h, p, 0);
+    if (rc == 0) {
+      e = cudaDeviceSynchronize();
+      if (e == cudaSuccess) e = cudaMemcpy(out_host, d_out, out_bytes, cudaMemcpyDeviceToHost);
+      int64_t nl = 0;
+      if (e == cudaSuccess) e = cudaMemcpy(&nl, d_logn, 8, cudaMemcpyDeviceToHost);
+      nl = std::min<int64_t>(nl, log_host ? log_cap : 0);
+      if (e == cudaSuccess && log_host && nl > 0)
+        e = cudaMemcpy(log_host, d_log, nl * 7 * 8, cudaMemcpyDeviceToHost);
+      if (n_logged) *n_logged = nl;
+    }
+  }
+  cudaFree(d_t); cudaFree(d_l); cudaFree(d_lp); cudaFree(d_off); cudaFree(d_out);
+  cudaFree(d_log); cudaFree(d_logn);
+  if (rc) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "sched_run_trace");
+  return SCHED_OK;
+}
+
+int sched_get_launch_info(sched_t h, sched_launch_info* out) {
+  if (!h || !out) return fail(SCHED_E_INVALID, "null argument");
+  if (int rc = prepare(h)) return rc;
+  out->grid = h->grid;
+  out->block = h->block;
+  out->warps_per_block = h->wpb;
+  out->shared_bytes = (int32_t)(h->wpb * h->warp_smem);
+  out->blocks_per_sm = h->blocks_per_sm;
+  out->sm_count = h->sm_count;
+  out->max_resident = (int32_t)h->Rc;
+  out->restart_cap = (int32_t)h->ring_cap;
+  return SCHED_OK;
+}
+
+void sched_destroy(sched_t h) {
+  if (!h) return;
+  cudaFree(h->d_cdf_thr);
+  cudaFree(h->d_cdf_val);
+  cudaFree(h->d_stage_info);
+  cudaFree(h->d_ring_a);
+  cudaFree(h->d_ring_e);
+  cudaFree(h->d_ring_llp);
+  cudaFree(h->d_counter);
+  cudaFree(h->d_out);
+  delete h;
+}
+
+}  // extern "C"

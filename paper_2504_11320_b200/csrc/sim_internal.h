@@ -1,0 +1,69 @@
+// sim_internal.h -- host <-> device parameter block of libsched (not part of
+// the public C ABI; see include/sched.h for that).
+#pragma once
+#include <stdint.h>
+
+namespace waitsim {
+
+constexpr int kMaxClasses = 32;
+constexpr int kMaxSegments = 32;
+constexpr int kLanes = 32;
+
+struct ClassParam {
+  double gap_scale;        // 1e12 / lambda (ticks per unit exponential); 0 = no arrivals
+  uint32_t l_off, l_n;     // CDF table slice (thresholds u64 [n-1], values u16 [n])
+  uint32_t lp_off, lp_n;
+};
+
+// Everything one launch needs, passed by value (lives in the constant bank).
+struct DevParams {
+  int32_t K;
+  int32_t policy;          // SCHED_WAIT / SCHED_NESTED / SCHED_FCFS
+  int32_t n_rings;         // restart rings per replication (WAIT: K, else 1)
+  int32_t n_seg;
+  int64_t d0_t, d1_t, T_t, M;
+  uint32_t thr[kMaxSegments];      // WAIT: per class, NESTED: per segment
+  uint32_t B, tok_budget;
+  uint32_t Rc;             // resident capacity per replication
+  uint32_t ring_cap;       // restart ring capacity (entries) per ring
+  uint32_t warp_smem;      // bytes of shared memory per warp
+  uint64_t seed;
+  uint64_t rep_begin;      // global index of local replication 0
+  uint32_t n_reps;
+  uint32_t trace_mode;
+  ClassParam cls[kMaxClasses];
+  const uint64_t* cdf_thr; // device
+  const uint16_t* cdf_val; // device
+  const uint8_t* stage_info; // NESTED: stage -> segment | entry<<7 (device)
+  // explicit traces (trace_mode): per (rep, class) slices of t / l / lp
+  const int64_t* tr_t;
+  const uint16_t* tr_l;
+  const uint16_t* tr_lp;
+  const int64_t* tr_off;   // [n_reps*K + 1]
+  // scratch
+  int64_t* ring_a;
+  int64_t* ring_e;
+  uint32_t* ring_llp;
+  uint32_t* work_counter;
+  // outputs
+  uint64_t* out;           // field-major [SCHED_NF][n_reps]
+  int64_t* log;            // trace mode: 7 int64 per batch of replication 0
+  int64_t log_cap;
+  int64_t* log_n;
+};
+
+// shared-memory bytes per warp for a given resident capacity / class count
+inline uint32_t warp_smem_bytes(uint32_t Rc, int K) {
+  uint32_t b = Rc * 16u;                    // residents SoA: a, l, l', s, meta
+  b += (uint32_t)K * (32u * 8u);            // visibility windows (t)
+  b += (uint32_t)K * (32u * 12u);           // admission windows (t, l, l')
+  b += (uint32_t)K * 48u;                   // per-class cursor state
+  b += 64u * 4u + 32u * 4u;                 // counters, per-segment ranks
+  return (b + 15u) & ~15u;
+}
+
+cudaError_t launch_sim(const DevParams& p, int grid, int block, size_t smem, cudaStream_t s);
+int sim_regs_per_thread(int policy, int trace);
+cudaError_t sim_occupancy(int policy, int trace, int block, size_t smem, int* blocks_per_sm);
+
+}  // namespace waitsim

@@ -1,0 +1,932 @@
+// sim_kernel.cu -- sm_100a kernel of the batched WAIT / Nested WAIT / FCFS
+// discrete-event simulation (arXiv 2504.11320).  One warp simulates one
+// replication; a persistent grid pulls replication indices from a global
+// counter.  Semantics: DESIGN.md §4 (event loop, policies, metrics), which
+// restates the paper passages cited inline.
+//
+// Layout per warp (shared memory, carved from dynamic smem):
+//   residents SoA in admission order: a[Rc] i64 (arrival tick), l[Rc],
+//     lp[Rc], s[Rc] (next stage to run), meta[Rc] (class | first-token<<8)
+//   per class: visibility window t[32], admission window t/l/lp[32]
+//   counters[64] (WAIT: residents per class; NESTED: [k] non-entry residents
+//     of segment k, [32+k] residents waiting at the entry stage of k),
+//   rank[32] (NESTED per-segment rank cursors).
+// Per-class cursor state lives in REGISTERS of lane c (broadcast by shfl).
+// Waiting prompts hold no KV: new arrivals are cursor ranges
+// [k_adm, k_vis) of the class's Philox stream, regenerated at admission;
+// evicted prompts go to per-FIFO restart rings in global memory.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/sched.h"
+#include "sim_internal.h"
+
+namespace waitsim {
+namespace {
+
+typedef unsigned __int128 u128;
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int64_t TMAX = INT64_MAX;
+constexpr uint16_t META_FT = 0x100;  // first output token already emitted
+
+// ------------------------------------------------------------- primitives
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // splitmix64 finaliser
+  z ^= z >> 30; z *= 0xbf58476d1ce4e5b9ull;
+  z ^= z >> 27; z *= 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  return z;
+}
+
+// Philox4x32-10 (Salmon et al., SC'11): 10 rounds, key bumped between rounds.
+__device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                              uint32_t k0, uint32_t k1, uint32_t& o0,
+                                              uint32_t& o1, uint32_t& o2, uint32_t& o3) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+  }
+  o0 = c0; o1 = c1; o2 = c2; o3 = c3;
+}
+
+// E = -ln U, U = (2 u52 + 1) 2^-53; every step one correctly rounded IEEE op
+// so the CPU oracle reproduces it bit for bit.
+__device__ __forceinline__ double neglog_bits(uint32_t x0, uint32_t x1) {
+  const uint64_t v = ((((uint64_t)x0 << 20) | (uint64_t)(x1 >> 12)) << 1) | 1ull;
+  int e = 63 - __clzll((long long)v);
+  // f = v * 2^-e in [1,2): exact, built from the bits
+  double f = __longlong_as_double(
+      (long long)((0x3FFull << 52) | ((v << (52 - e)) & 0xFFFFFFFFFFFFFull)));
+  if (f > 0x1.6a09e667f3bcdp+0) { f = __dmul_rn(f, 0.5); e += 1; }
+  const double s = __ddiv_rn(__dsub_rn(f, 1.0), __dadd_rn(f, 1.0));
+  const double z = __dmul_rn(s, s);
+  double P = 1.0 / 19.0;
+  P = __dadd_rn(__dmul_rn(P, z), 1.0 / 17.0);
+  P = __dadd_rn(__dmul_rn(P, z), 1.0 / 15.0);
+  P = __dadd_rn(__dmul_rn(P, z), 1.0 / 13.0);
+  P = __dadd_rn(__dmul_rn(P, z), 1.0 / 11.0);
+  P = __dadd_rn(__dmul_rn(P, z), 1.0 / 9.0);
+  P = __dadd_rn(__dmul_rn(P, z), 1.0 / 7.0);
+  P = __dadd_rn(__dmul_rn(P, z), 1.0 / 5.0);
+  P = __dadd_rn(__dmul_rn(P, z), 1.0 / 3.0);
+  P = __dadd_rn(__dmul_rn(P, z), 1.0);
+  const double lnf = __dmul_rn(__dadd_rn(s, s), P);
+  const double dn = (double)(e - 53);
+  const double ln2_hi = __longlong_as_double(0x3fe62e42fee00000ll);
+  const double ln2_lo = __longlong_as_double(0x3dea39ef35793c76ll);
+  const double lnU = __dadd_rn(__dmul_rn(dn, ln2_hi), __dadd_rn(__dmul_rn(dn, ln2_lo), lnf));
+  return -lnU;
+}
+
+// inverse-CDF of an integer-weight table: idx = min{i : x < thr_i}
+__device__ __forceinline__ uint32_t cdf_sample(const uint64_t* __restrict__ thr,
+                                               const uint16_t* __restrict__ val, uint32_t off,
+                                               uint32_t n, uint32_t x) {
+  if (n == 1) return __ldg(val + off);
+  uint32_t lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(thr + off + mid) > (uint64_t)x) hi = mid; else lo = mid + 1;
+  }
+  return __ldg(val + off + lo);
+}
+
+__device__ __forceinline__ int64_t warp_incl_scan_i64(int64_t x, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int64_t y = __shfl_up_sync(FULL, x, d);
+    if (lane >= d) x += y;
+  }
+  return x;
+}
+__device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t x, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, x, d);
+    if (lane >= d) x += y;
+  }
+  return x;
+}
+__device__ __forceinline__ u128 warp_sum_u128(u128 x) {
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) {
+    const uint64_t lo = __shfl_xor_sync(FULL, (uint64_t)x, d);
+    const uint64_t hi = __shfl_xor_sync(FULL, (uint64_t)(x >> 64), d);
+    x += ((u128)hi << 64) | lo;
+  }
+  return x;
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ int64_t bcast64(int64_t v, int src) { return __shfl_sync(FULL, v, src); }
+__device__ __forceinline__ uint32_t bcast32(uint32_t v, int src) { return __shfl_sync(FULL, v, src); }
+
+// ------------------------------------------------------------- the warp sim
+template <int POL, bool TRACE>
+struct WarpSim {
+  const DevParams& P;
+  const int lane;
+  // shared-memory views (this warp's slice)
+  int64_t* ra; uint16_t* rl; uint16_t* rlp; uint16_t* rs; uint16_t* rm;
+  int64_t* vt;                       // [K][32] visibility windows
+  int64_t* at; uint16_t* al; uint16_t* alp;  // [K][32] admission windows
+  uint32_t* cnt;                     // [64]
+  uint32_t* rank;                    // [32]
+  size_t ring_base;                  // first ring entry of this warp slot
+
+  // per-class cursor state, lane c holds class c (and ring c for WAIT; ring 0
+  // otherwise).  vbase/abase: first arrival index held by the window;
+  // vprev/aprev: tick of arrival (base - 1), the scan carry.
+  uint32_t k_vis, vbase, k_adm, abase, rhead, rtail;
+  int64_t vprev, aprev;
+  uint32_t sv_k, sv_rhead;           // saved admission cursor (drop/rewind)
+  int64_t sv_prev;
+
+  // replication
+  uint32_t rep, rglob;
+  int64_t now, KV;
+  uint32_t n_res, n_new, status;
+  int64_t sum_new_l;
+  uint64_t arrivals, admitted, completed, completed_after_T, completed_tokens, first_tokens,
+      batches, request_steps, prefill_steps, evictions, cbi, sum_waiting;
+  int64_t busy, idle, max_kv;
+  uint64_t h;
+  u128 acc_lat, acc_ttft, acc_arr, acc_arr_done;  // lane-local partial sums
+  int64_t log_n;
+  // per-epoch plan
+  uint32_t Qmask;     // WAIT: qualifying classes
+  int kstar;          // NESTED: last active segment
+  uint32_t n_plan_res;
+
+  __device__ WarpSim(const DevParams& p, unsigned char* base, int lane_, size_t rb)
+      : P(p), lane(lane_), ring_base(rb) {
+    const uint32_t Rc = p.Rc;
+    ra = (int64_t*)base;
+    vt = ra + Rc;
+    at = vt + p.K * 32;
+    rl = (uint16_t*)(at + p.K * 32);
+    rlp = rl + Rc;
+    rs = rlp + Rc;
+    rm = rs + Rc;
+    al = rm + Rc;
+    alp = al + p.K * 32;
+    cnt = (uint32_t*)(((uintptr_t)(alp + p.K * 32) + 15) & ~(uintptr_t)15);
+    rank = cnt + 64;
+  }
+
+  __device__ __forceinline__ int ring_of(int c) const { return POL == SCHED_WAIT ? c : 0; }
+  __device__ __forceinline__ size_t ring_slot(int q, uint32_t pos) const {
+    return ring_base + (size_t)q * P.ring_cap + (pos % P.ring_cap);
+  }
+
+  // ---------------------------------------------------- S1 arrival windows
+  // Fill the 32 arrivals [base, base+32) of class c: lane i draws arrival
+  // base+i from Philox counter (k, r, c, 0), gaps are
+  // turned into ticks by an inclusive warp scan on top of `prev`.
+  template <bool WITH_LEN>
+  __device__ __forceinline__ void fill(int c, uint32_t base, int64_t prev, int64_t* wt,
+                                       uint16_t* wl, uint16_t* wlp) {
+    const uint32_t k = base + lane;
+    int64_t t;
+    uint32_t l = 1, lp = 1;
+    if (TRACE) {
+      const int64_t beg = P.tr_off[(size_t)rep * P.K + c];
+      const int64_t end = P.tr_off[(size_t)rep * P.K + c + 1];
+      if (beg + (int64_t)k < end) {
+        t = P.tr_t[beg + k];
+        if (WITH_LEN) { l = P.tr_l[beg + k]; lp = P.tr_lp[beg + k]; }
+      } else {
+        t = TMAX;
+      }
+    } else {
+      const double gs = P.cls[c].gap_scale;
+      if (gs == 0.0) {
+        t = TMAX;
+      } else {
+        uint32_t x0, x1, x2, x3;
+        philox4x32_10(k, rglob, (uint32_t)c, 0u, (uint32_t)P.seed, (uint32_t)(P.seed >> 32),
+                      x0, x1, x2, x3);
+        const int64_t gap = __double2ll_rz(__dmul_rn(neglog_bits(x0, x1), gs));
+        t = prev + warp_incl_scan_i64(gap, lane);
+        if (WITH_LEN) {
+          l = cdf_sample(P.cdf_thr, P.cdf_val, P.cls[c].l_off, P.cls[c].l_n, x2);
+          lp = cdf_sample(P.cdf_thr, P.cdf_val, P.cls[c].lp_off, P.cls[c].lp_n, x3);
+        }
+      }
+    }
+    __syncwarp();
+    wt[c * 32 + lane] = t;
+    if (WITH_LEN) { wl[c * 32 + lane] = (uint16_t)l; wlp[c * 32 + lane] = (uint16_t)lp; }
+    __syncwarp();
+  }
+
+  // class-c cursor fields (uniform broadcast from lane c)
+  __device__ __forceinline__ uint32_t kvis(int c) const { return bcast32(k_vis, c); }
+  __device__ __forceinline__ uint32_t kadm(int c) const { return bcast32(k_adm, c); }
+  __device__ __forceinline__ uint32_t rcount(int q) const { return bcast32(rtail, q) - bcast32(rhead, q); }
+
+  // ensure class c's admission window holds arrival k_adm(c)
+  __device__ __forceinline__ void adm_window(int c) {
+    const uint32_t ka = kadm(c), ab = bcast32(abase, c);
+    if (ka == ab + 32) {
+      const int64_t carry = at[c * 32 + 31];
+      fill<true>(c, ka, carry, at, al, alp);
+      if (lane == c) { abase = ka; aprev = carry; }
+    }
+  }
+
+  // ------------------------------------------------------ S2 ingestion
+  // INGEST (DESIGN.md §4.4 step 1): arrivals with t <= now and t < T become
+  // visible (join their FIFO).  Cursor only: count + arrival-time sum.
+  __device__ void ingest() {
+    for (int c = 0; c < P.K; ++c) {
+      for (;;) {
+        uint32_t kv = kvis(c), vb = bcast32(vbase, c);
+        if (kv == vb + 32) {
+          const int64_t carry = vt[c * 32 + 31];
+          fill<false>(c, kv, carry, vt, nullptr, nullptr);
+          if (lane == c) { vbase = kv; vprev = carry; }
+          vb = kv;
+        }
+        const uint32_t j = kv - vb;
+        const int64_t t = vt[c * 32 + lane];
+        const bool vis = (uint32_t)lane >= j && t <= now && t < P.T_t;
+        const uint32_t n = __popc(__ballot_sync(FULL, vis));
+        if (vis) acc_arr += (u128)(uint64_t)t;
+        arrivals += n;
+        if (lane == c) k_vis += n;
+        if (j + n < 32) break;
+      }
+    }
+  }
+
+  // next not-yet-visible arrival tick (< T), TMAX if none
+  __device__ int64_t next_arrival() const {
+    int64_t best = TMAX;
+    for (int c = 0; c < P.K; ++c) {
+      const int64_t t = vt[c * 32 + (kvis(c) - bcast32(vbase, c))];
+      if (t < P.T_t && t < best) best = t;
+    }
+    return best;
+  }
+
+  __device__ __forceinline__ uint32_t waiting_class(int c) const {
+    return kvis(c) - kadm(c) + (POL == SCHED_WAIT ? rcount(c) : 0u);
+  }
+  __device__ uint32_t waiting_total() const {
+    uint32_t w = 0;
+    for (int c = 0; c < P.K; ++c) w += kvis(c) - kadm(c);
+    const int nr = POL == SCHED_WAIT ? P.K : 1;
+    for (int q = 0; q < nr; ++q) w += rcount(q);
+    return w;
+  }
+
+  // ------------------------------------------------------- admissions
+  // stage one prompt at resident slot n_res + n_new (prefill -> stage 1)
+  __device__ __forceinline__ bool stage_one(int64_t a, uint32_t l, uint32_t lp, uint16_t meta) {
+    const uint32_t i = n_res + n_new;
+    if (i >= P.Rc) { status = 1; return false; }
+    if (lane == 0) { ra[i] = a; rl[i] = (uint16_t)l; rlp[i] = (uint16_t)lp; rs[i] = 1; rm[i] = meta; }
+    __syncwarp();
+    ++n_new;
+    sum_new_l += l;
+    return true;
+  }
+  // take the arrival at the head of class c's cursor
+  __device__ __forceinline__ bool take_arrival(int c) {
+    adm_window(c);
+    const uint32_t j = kadm(c) - bcast32(abase, c);
+    const int64_t t = at[c * 32 + j];
+    const uint32_t l = al[c * 32 + j], lp = alp[c * 32 + j];
+    if (!stage_one(t, l, lp, (uint16_t)c)) return false;
+    if (lane == c) ++k_adm;
+    return true;
+  }
+  __device__ __forceinline__ bool take_restart(int q) {
+    const uint32_t h0 = bcast32(rhead, q);
+    const size_t e = ring_slot(q, h0);
+    const int64_t a = P.ring_a[e];
+    const uint32_t llp = P.ring_llp[e];
+    const uint16_t meta = (uint16_t)((POL == SCHED_WAIT ? q : 0) | ((llp >> 31) ? META_FT : 0));
+    if (!stage_one(a, llp & 0xFFFFu, (llp >> 16) & 0x7FFFu, meta)) return false;
+    if (lane == q) ++rhead;
+    return true;
+  }
+  // Which source holds the FIFO head?  Arrivals are ordered (t, class);
+  // a restart evicted at tick e precedes exactly the arrivals with t > e
+  // (restarts join the tail after same-tick arrivals).
+  // Returns class index, 32 for the restart ring, -1 if empty.
+  __device__ int head_source_merged(int64_t* l_out) {
+    int best = -1;
+    int64_t bt = TMAX;
+    for (int c = 0; c < P.K; ++c) {
+      if (kadm(c) < kvis(c)) {
+        adm_window(c);
+        const int64_t t = at[c * 32 + (kadm(c) - bcast32(abase, c))];
+        if (t < bt) { bt = t; best = c; }
+      }
+    }
+    if (rcount(0) > 0) {
+      const size_t e = ring_slot(0, bcast32(rhead, 0));
+      if (best < 0 || P.ring_e[e] < bt) {
+        if (l_out) *l_out = P.ring_llp[e] & 0xFFFFu;
+        return 32;
+      }
+    }
+    if (best >= 0 && l_out) *l_out = al[best * 32 + (kadm(best) - bcast32(abase, best))];
+    return best;
+  }
+  __device__ int head_source_class(int c) {
+    const bool arr = kadm(c) < kvis(c);
+    int64_t t = TMAX;
+    if (arr) { adm_window(c); t = at[c * 32 + (kadm(c) - bcast32(abase, c))]; }
+    if (rcount(c) > 0 && (!arr || P.ring_e[ring_slot(c, bcast32(rhead, c))] < t)) return 32;
+    return arr ? c : -1;
+  }
+
+  // bulk take of `cnt_` arrivals of class c (no restarts pending): lane-parallel
+  __device__ bool take_bulk(int c, uint32_t cnt_) {
+    while (cnt_ > 0) {
+      adm_window(c);
+      const uint32_t j = kadm(c) - bcast32(abase, c);
+      const uint32_t take = min(cnt_, 32u - j);
+      if (n_res + n_new + take > P.Rc) { status = 1; return false; }
+      const bool act = (uint32_t)lane < take;
+      uint32_t l = 0;
+      if (act) {
+        const uint32_t d = n_res + n_new + lane;
+        l = al[c * 32 + j + lane];
+        ra[d] = at[c * 32 + j + lane];
+        rl[d] = (uint16_t)l;
+        rlp[d] = alp[c * 32 + j + lane];
+        rs[d] = 1;
+        rm[d] = (uint16_t)c;
+      }
+      __syncwarp();
+      sum_new_l += __reduce_add_sync(FULL, l);
+      n_new += take;
+      if (lane == c) k_adm += take;
+      cnt_ -= take;
+    }
+    return true;
+  }
+
+  // save / restore the admission cursors (rare: a drop after eviction)
+  __device__ void save_cursors() {
+    sv_k = k_adm;
+    sv_rhead = rhead;
+    const uint32_t j = k_adm - abase;  // lane-local (own class)
+    sv_prev = aprev;
+    // tick of arrival k_adm-1: window entry j-1 if j > 0 (read by every lane
+    // of its own class slot; lanes >= K hold garbage and never use it)
+    if (lane < P.K && j > 0 && j <= 32) sv_prev = at[lane * 32 + j - 1];
+  }
+  __device__ void restore_cursors() {
+    for (int c = 0; c < P.K; ++c) {
+      const uint32_t k = bcast32(sv_k, c);
+      const int64_t pv = bcast64(sv_prev, c);
+      const uint32_t ab = bcast32(abase, c);
+      if (!(k >= ab && k <= ab + 32)) {
+        fill<true>(c, k, pv, at, al, alp);
+        if (lane == c) { abase = k; aprev = pv; }
+      }
+      if (lane == c) k_adm = k;
+    }
+    rhead = sv_rhead;
+  }
+
+  // ---------------------------------------------------- S3 decide + take
+  // Returns false for "no batch".  limit = max number of new admissions
+  // (used when re-taking after a drop).
+  __device__ bool take_wait(uint32_t limit) {
+    for (int c = 0; c < P.K && limit > 0; ++c) {
+      if (!((Qmask >> c) & 1u)) continue;
+      uint32_t want = min(P.thr[c], limit);
+      limit -= want;
+      if (rcount(c) == 0) {
+        if (!take_bulk(c, want)) return false;
+      } else {
+        while (want-- > 0) {
+          const int src = head_source_class(c);
+          if (!(src == 32 ? take_restart(c) : take_arrival(c))) return false;
+        }
+      }
+    }
+    return true;
+  }
+  __device__ bool take_merged_n(uint32_t want) {
+    if (P.K == 1 && rcount(0) == 0) return take_bulk(0, want);
+    while (want-- > 0) {
+      const int src = head_source_merged(nullptr);
+      if (!(src == 32 ? take_restart(0) : take_arrival(src))) return false;
+    }
+    return true;
+  }
+  __device__ bool take_fcfs() {
+    if (P.K == 1 && rcount(0) == 0) {
+      // lane-parallel admission scan over the cursor window
+      for (;;) {
+        const uint32_t avail_all = kvis(0) - kadm(0);
+        if (avail_all == 0) break;
+        adm_window(0);
+        const uint32_t j = kadm(0) - bcast32(abase, 0);
+        const uint32_t avail = min(avail_all, 32u - j);
+        const bool act = (uint32_t)lane < avail;
+        const uint32_t l = act ? al[j + lane] : 0u;
+        const uint32_t pre = warp_incl_scan_u32(l, lane);
+        const bool ok = act && (n_res + n_new + lane < P.B) &&
+                        (KV + sum_new_l + (int64_t)pre <= P.M) &&
+                        (P.tok_budget == 0 || sum_new_l + (int64_t)pre <= (int64_t)P.tok_budget);
+        const uint32_t okm = __ballot_sync(FULL, ok);
+        const uint32_t take = okm == FULL ? 32u : (uint32_t)__ffs(~okm) - 1;  // ok lanes: a prefix
+        if (take == 0) break;
+        if (n_res + n_new + take > P.Rc) { status = 1; return false; }
+        if ((uint32_t)lane < take) {
+          const uint32_t d = n_res + n_new + lane;
+          ra[d] = at[j + lane]; rl[d] = (uint16_t)l; rlp[d] = alp[j + lane]; rs[d] = 1; rm[d] = 0;
+        }
+        __syncwarp();
+        sum_new_l += __shfl_sync(FULL, pre, take - 1);
+        n_new += take;
+        if (lane == 0) k_adm += take;
+        if (take < avail) break;
+      }
+      return true;
+    }
+    for (;;) {
+      if (n_res + n_new >= P.B) break;
+      int64_t l = 0;
+      const int src = head_source_merged(&l);
+      if (src < 0) break;
+      if (KV + sum_new_l + l > P.M) break;
+      if (P.tok_budget != 0 && sum_new_l + l > (int64_t)P.tok_budget) break;
+      if (!(src == 32 ? take_restart(0) : take_arrival(src))) return false;
+    }
+    return true;
+  }
+
+  __device__ bool decide() {
+    n_new = 0;
+    sum_new_l = 0;
+    if (POL == SCHED_WAIT) {
+      // Algorithm 1: type j joins the batch iff n_j0 >= n_j;
+      // all residents of qualifying types ride along (line 1490, invariant P14)
+      uint32_t q = 0, npr = 0;
+      if (lane < P.K) {
+        const uint32_t w = k_vis - k_adm + (rtail - rhead);
+        if (w >= P.thr[lane]) { q = 1; npr = cnt[lane]; }
+      }
+      Qmask = __ballot_sync(FULL, q);
+      if (!Qmask) return false;
+      n_plan_res = __reduce_add_sync(FULL, npr);
+      save_cursors();
+      return take_wait(0xFFFFFFFFu);
+    } else if (POL == SCHED_NESTED) {
+      // Algorithm 2: largest k with Q_{k',entry} >= n_k' for all k' <= k
+      // (PAPER.md:1640); batch min{n_k, Q_{k,s}} per stage (line 1642)
+      if (waiting_total() < P.thr[0]) return false;
+      int ks = 0;
+      for (int k = 1; k < P.n_seg; ++k) {
+        if (cnt[32 + k] >= P.thr[k]) ks = k; else break;
+      }
+      kstar = ks;
+      uint32_t npr = 0;
+      if (lane <= ks) {
+        npr = cnt[lane];
+        if (lane >= 1) npr += min(cnt[32 + lane], P.thr[lane]);
+      }
+      n_plan_res = __reduce_add_sync(FULL, npr);
+      save_cursors();
+      return take_merged_n(P.thr[0]);
+    } else {
+      // FCFS new-first (R15)
+      n_plan_res = n_res;
+      if (!take_fcfs()) return false;
+      return n_res + n_new > 0;
+    }
+  }
+
+  // membership of resident i (chunk-parallel), NESTED rank bookkeeping in
+  // rank[] (head order) -- only valid inside execute()
+  __device__ __forceinline__ bool in_plan_simple(uint16_t meta) const {
+    if (POL == SCHED_FCFS) return true;
+    return (Qmask >> (meta & 0xFF)) & 1u;
+  }
+
+  // --------------------------------------- S4 memory check / LIFO eviction
+  __device__ void memory(uint32_t& n_evict, int64_t& peak) {
+    peak = KV + (int64_t)n_plan_res + sum_new_l;
+    if (peak <= P.M) return;
+    int64_t excess = peak - P.M;
+    const uint32_t old_n = n_res;
+    if (POL == SCHED_NESTED) { if (lane < 32) rank[lane] = 0; __syncwarp(); }
+    while (excess > 0 && n_res > 0) {
+      const int idx = (int)n_res - 1 - lane;  // lane 0 = last admitted
+      const bool valid = idx >= 0;
+      uint32_t l = 0, lp = 0, s = 0, meta = 0;
+      int64_t a = 0;
+      if (valid) { l = rl[idx]; lp = rlp[idx]; s = rs[idx]; meta = rm[idx]; a = ra[idx]; }
+      uint32_t inp = 0;
+      if (valid) {
+        if (POL != SCHED_NESTED) inp = in_plan_simple((uint16_t)meta);
+      }
+      if (POL == SCHED_NESTED) {
+        const uint32_t info = valid ? __ldg(P.stage_info + s) : 0u;
+        const int seg = info & 0x7F;
+        const bool entry = valid && (info >> 7) && seg <= kstar;
+        const uint32_t key = entry ? s : (0x10000u + lane);
+        const uint32_t grp = __match_any_sync(FULL, key);
+        if (valid && seg <= kstar) {
+          if (entry) {
+            const uint32_t after = rank[seg] + __popc(grp & lanemask_lt());
+            const uint32_t r = cnt[32 + seg] - 1 - after;  // rank from the head
+            inp = r < P.thr[seg];
+          } else {
+            inp = 1;
+          }
+        }
+        __syncwarp();
+        if (entry && (grp & lanemask_lt()) == 0) rank[seg] += __popc(grp);
+        __syncwarp();
+      }
+      const uint32_t f = valid ? (l + s - 1 + inp) : 0u;
+      const uint32_t cum = warp_incl_scan_u32(f, lane);
+      const uint32_t hit = __ballot_sync(FULL, valid && (int64_t)cum >= excess);
+      const uint32_t ne = hit ? (uint32_t)__ffs(hit) : min(n_res, 32u);
+      const bool ev = (uint32_t)lane < ne;
+      // restart records in eviction order (re-enter the queue)
+      const int q = POL == SCHED_WAIT ? (int)(meta & 0xFF) : 0;
+      const uint32_t key = ev ? (uint32_t)q : (0x100u + lane);
+      const uint32_t grp = __match_any_sync(FULL, key);
+      const uint32_t before = __popc(grp & lanemask_lt());
+      const uint32_t tail_q = __shfl_sync(FULL, rtail, q);
+      const uint32_t head_q = __shfl_sync(FULL, rhead, q);
+      const bool overflow = ev && (tail_q - head_q + before + 1 > P.ring_cap);
+      if (__any_sync(FULL, overflow)) { status = 2; return; }
+      if (ev) {
+        const size_t e = ring_slot(q, tail_q + before);
+        P.ring_a[e] = a;
+        P.ring_e[e] = now;
+        P.ring_llp[e] = l | (lp << 16) | ((meta & META_FT) ? 0x80000000u : 0u);
+      }
+      // advance ring tails (lane q owns ring q)
+      if (POL == SCHED_WAIT) {
+        for (int c = 0; c < P.K; ++c) {
+          const uint32_t m = __ballot_sync(FULL, ev && q == c);
+          if (lane == c) rtail += __popc(m);
+        }
+      } else if (lane == 0) {
+        rtail += ne;
+      }
+      excess -= (int64_t)__reduce_add_sync(FULL, ev ? f : 0u);
+      KV -= (int64_t)__reduce_add_sync(FULL, ev ? (l + s - 1) : 0u);
+      n_plan_res -= __reduce_add_sync(FULL, ev ? inp : 0u);
+      n_res -= ne;
+      evictions += ne;
+      n_evict += ne;
+    }
+    // close the gap between the surviving residents and the staged admissions
+    if (n_res != old_n && n_new > 0) {
+      for (uint32_t o = 0; o < n_new; o += 32) {
+        const uint32_t i = o + lane;
+        int64_t a = 0; uint16_t l = 0, lp = 0, s = 0, m = 0;
+        if (i < n_new) { a = ra[old_n + i]; l = rl[old_n + i]; lp = rlp[old_n + i]; s = rs[old_n + i]; m = rm[old_n + i]; }
+        __syncwarp();
+        if (i < n_new) { ra[n_res + i] = a; rl[n_res + i] = l; rlp[n_res + i] = lp; rs[n_res + i] = s; rm[n_res + i] = m; }
+        __syncwarp();
+      }
+    }
+    if (excess > 0) {
+      // no residents left: drop the latest new admissions (they stay queued)
+      uint32_t keep = n_new;
+      while (excess > 0 && keep > 0) { excess -= rl[n_res + keep - 1]; --keep; }
+      restore_cursors();
+      n_new = 0;
+      sum_new_l = 0;
+      if (POL == SCHED_WAIT) take_wait(keep);
+      else take_merged_n(keep);  // FCFS never reaches here (admission bound)
+    }
+    peak = P.M + excess;
+  }
+
+  // ------------------------------------------------------ S5 execute
+  // One pass over residents (+ the staged admissions) in admission order:
+  // per-member update, completions, compaction and counter recount.
+  __device__ void execute(uint32_t n_evict, int64_t peak, uint32_t waiting) {
+    const uint32_t n_tot = n_res + n_new;
+    if (POL != SCHED_FCFS) {
+      if (lane < 32) { cnt[lane] = 0; cnt[32 + lane] = 0; rank[lane] = 0; }
+      __syncwarp();
+    }
+    uint32_t tok = 0, n_done = 0, done_tok = 0, n_ft = 0, kv_free = 0, grow = 0;
+    uint64_t done_a = 0, ft_a = 0;
+    uint32_t wp = 0;
+    for (uint32_t base = 0; base < n_tot; base += 32) {
+      const uint32_t i = base + lane;
+      const bool valid = i < n_tot;
+      const bool fresh = i >= n_res;
+      int64_t a = 0;
+      uint32_t l = 0, lp = 0, s = 0, meta = 0;
+      if (valid) { a = ra[i]; l = rl[i]; lp = rlp[i]; s = rs[i]; meta = rm[i]; }
+      bool inp = false;
+      if (POL == SCHED_NESTED) {
+        const uint32_t info = (valid && !fresh) ? __ldg(P.stage_info + s) : 0x7Fu;
+        const int seg = info & 0x7F;
+        const bool act = valid && !fresh && seg <= kstar;
+        const bool entry = act && (info >> 7);
+        const uint32_t key = entry ? s : (0x10000u + lane);
+        const uint32_t grp = __match_any_sync(FULL, key);
+        if (act) inp = entry ? (rank[seg] + __popc(grp & lanemask_lt()) < P.thr[seg]) : true;
+        __syncwarp();
+        if (entry && (grp & lanemask_lt()) == 0) rank[seg] += __popc(grp);
+      } else {
+        inp = valid && !fresh && in_plan_simple((uint16_t)meta);
+      }
+      bool keep = valid;
+      uint32_t ns = s;
+      if (inp) {
+        tok += l + s;
+        // the stage-1 iteration emits the first output token
+        if (s == 1 && !(meta & META_FT)) { meta |= META_FT; ++n_ft; ft_a += (uint64_t)a; }
+        if (s == lp) {
+          // stage l' done: complete, free KV
+          keep = false;
+          kv_free += l + lp - 1;
+          ++n_done;
+          done_tok += lp;
+          done_a += (uint64_t)a;
+        } else {
+          ns = s + 1;
+          ++grow;
+        }
+      }
+      const uint32_t km = __ballot_sync(FULL, keep);
+      const uint32_t d = wp + __popc(km & lanemask_lt());
+      __syncwarp();
+      if (keep) {
+        if (d != i) { ra[d] = a; rl[d] = (uint16_t)l; rlp[d] = (uint16_t)lp; }
+        rs[d] = (uint16_t)ns;
+        rm[d] = (uint16_t)meta;
+      }
+      if (POL != SCHED_FCFS) {
+        uint32_t key;
+        if (POL == SCHED_WAIT) {
+          key = keep ? (meta & 0xFF) : (0x100u + lane);
+        } else {
+          const uint32_t info = keep ? __ldg(P.stage_info + ns) : 0u;
+          key = keep ? ((info & 0x7F) + ((info >> 7) ? 32u : 0u)) : (0x100u + lane);
+        }
+        const uint32_t grp = __match_any_sync(FULL, key);
+        if (keep && (grp & lanemask_lt()) == 0) cnt[key] += __popc(grp);
+      }
+      wp += __popc(km);
+      __syncwarp();
+    }
+    // warp-uniform batch totals
+    tok = __reduce_add_sync(FULL, tok);
+    const uint32_t nd = __reduce_add_sync(FULL, n_done);
+    const uint32_t nf = __reduce_add_sync(FULL, n_ft);
+    const uint32_t dtok = __reduce_add_sync(FULL, done_tok);
+    const uint32_t kvf = __reduce_add_sync(FULL, kv_free);
+    const uint32_t gr = __reduce_add_sync(FULL, grow);
+    const int64_t tokens = (int64_t)tok + sum_new_l;
+    // tau = d0 + d1 * (sum prefill l + sum decode (l+s))
+    const int64_t tau = P.d0_t + P.d1_t * tokens;
+    const int64_t t_end = now + tau;
+    if (t_end <= P.T_t) {
+      acc_lat += (u128)((uint64_t)n_done * (uint64_t)t_end - done_a);
+      acc_ttft += (u128)((uint64_t)n_ft * (uint64_t)t_end - ft_a);
+      acc_arr_done += (u128)done_a;
+      completed += nd;
+      completed_tokens += dtok;
+      first_tokens += nf;
+      cbi += (uint64_t)nd * batches;
+    } else {
+      completed_after_T += nd;
+    }
+    KV += (int64_t)gr - (int64_t)kvf + sum_new_l;
+    const uint32_t plan_size = n_plan_res + n_new;
+    if (TRACE && rep == 0 && lane == 0 && log_n < P.log_cap) {
+      int64_t* e = P.log + 7 * log_n;
+      e[0] = now; e[1] = plan_size; e[2] = tokens; e[3] = nd; e[4] = n_evict; e[5] = n_new; e[6] = peak;
+    }
+    if (TRACE && rep == 0) ++log_n;
+    h = mix64(h ^ (uint64_t)now);
+    h = mix64(h ^ ((uint64_t)plan_size | ((uint64_t)tokens << 32)));
+    h = mix64(h ^ ((uint64_t)nd | ((uint64_t)n_evict << 20) | ((uint64_t)n_new << 40)));
+    request_steps += plan_size;
+    prefill_steps += n_new;
+    admitted += n_new;
+    busy += tau;
+    if (peak > max_kv) max_kv = peak;
+    sum_waiting += waiting;
+    ++batches;
+    n_res = wp;
+    n_new = 0;
+    now = t_end;
+  }
+
+  // counters after an epoch whose plan emptied (evictions but no batch)
+  __device__ void recount() {
+    if (POL == SCHED_FCFS) return;
+    if (lane < 32) { cnt[lane] = 0; cnt[32 + lane] = 0; }
+    __syncwarp();
+    for (uint32_t base = 0; base < n_res; base += 32) {
+      const uint32_t i = base + lane;
+      const bool valid = i < n_res;
+      uint32_t key = 0x100u + lane;
+      if (valid) {
+        if (POL == SCHED_WAIT) key = rm[i] & 0xFF;
+        else { const uint32_t info = __ldg(P.stage_info + rs[i]); key = (info & 0x7F) + ((info >> 7) ? 32u : 0u); }
+      }
+      const uint32_t grp = __match_any_sync(FULL, key);
+      if (valid && (grp & lanemask_lt()) == 0) cnt[key] += __popc(grp);
+      __syncwarp();
+    }
+  }
+
+  // ------------------------------------------------------------ run
+  __device__ void run(uint32_t rep_) {
+    rep = rep_;
+    rglob = (uint32_t)(P.rep_begin + rep_);
+    const uint64_t seed = TRACE ? 0ull : P.seed;
+    h = mix64(seed ^ ((uint64_t)(TRACE ? rep_ : rglob) * 0x9E3779B97F4A7C15ull));
+    now = 0; KV = 0; n_res = 0; n_new = 0; status = 0; sum_new_l = 0;
+    arrivals = admitted = completed = completed_after_T = completed_tokens = first_tokens = 0;
+    batches = request_steps = prefill_steps = evictions = cbi = sum_waiting = 0;
+    busy = idle = max_kv = 0;
+    acc_lat = acc_ttft = acc_arr = acc_arr_done = 0;
+    log_n = 0;
+    k_vis = vbase = k_adm = abase = rhead = rtail = 0;
+    vprev = aprev = 0;
+    for (int c = 0; c < P.K; ++c) {
+      fill<false>(c, 0, 0, vt, nullptr, nullptr);
+      fill<true>(c, 0, 0, at, al, alp);
+    }
+    if (POL != SCHED_FCFS) {
+      if (lane < 32) { cnt[lane] = 0; cnt[32 + lane] = 0; }
+      __syncwarp();
+    }
+    for (;;) {
+      ingest();
+      if (now >= P.T_t) break;                     // STOP
+      const uint32_t waiting = waiting_total();
+      bool go = decide();
+      if (status) break;
+      uint32_t n_evict = 0;
+      int64_t peak = 0;
+      if (go) {
+        memory(n_evict, peak);
+        if (status) break;
+        if (n_plan_res + n_new == 0) { go = false; recount(); }
+      }
+      if (!go) {
+        const int64_t nt = next_arrival();
+        if (nt == TMAX) break;
+        idle += nt - now;
+        now = nt;
+        continue;
+      }
+      execute(n_evict, peak, waiting);
+    }
+    finish();
+  }
+
+  __device__ void finish() {
+    const uint32_t waiting = waiting_total();
+    const u128 lat = warp_sum_u128(acc_lat);
+    const u128 ttft = warp_sum_u128(acc_ttft);
+    const u128 arr = warp_sum_u128(acc_arr);
+    const u128 arr_done = warp_sum_u128(acc_arr_done);
+    const u128 soj = lat + (u128)(arrivals - completed) * (u128)(uint64_t)P.T_t - (arr - arr_done);
+    uint64_t v = 0;
+    switch (lane) {
+      case SCHED_F_ARRIVALS: v = arrivals; break;
+      case SCHED_F_ADMITTED: v = admitted; break;
+      case SCHED_F_COMPLETED: v = completed; break;
+      case SCHED_F_COMPLETED_AFTER_T: v = completed_after_T; break;
+      case SCHED_F_COMPLETED_TOKENS: v = completed_tokens; break;
+      case SCHED_F_FIRST_TOKENS: v = first_tokens; break;
+      case SCHED_F_BATCHES: v = batches; break;
+      case SCHED_F_REQUEST_STEPS: v = request_steps; break;
+      case SCHED_F_PREFILL_STEPS: v = prefill_steps; break;
+      case SCHED_F_EVICTIONS: v = evictions; break;
+      case SCHED_F_BUSY_TICKS: v = (uint64_t)busy; break;
+      case SCHED_F_IDLE_TICKS: v = (uint64_t)idle; break;
+      case SCHED_F_LAT_LO: v = (uint64_t)lat; break;
+      case SCHED_F_LAT_HI: v = (uint64_t)(lat >> 64); break;
+      case SCHED_F_TTFT_LO: v = (uint64_t)ttft; break;
+      case SCHED_F_TTFT_HI: v = (uint64_t)(ttft >> 64); break;
+      case SCHED_F_SOJ_LO: v = (uint64_t)soj; break;
+      case SCHED_F_SOJ_HI: v = (uint64_t)(soj >> 64); break;
+      case SCHED_F_COMPLETION_BATCH_IDX: v = cbi; break;
+      case SCHED_F_MAX_KV_PEAK: v = (uint64_t)max_kv; break;
+      case SCHED_F_FINAL_WAITING: v = waiting; break;
+      case SCHED_F_FINAL_RESIDENT: v = n_res; break;
+      case SCHED_F_TRAJ_HASH: v = h; break;
+      case SCHED_F_STATUS: v = status; break;
+      case SCHED_F_NOW_STOP: v = (uint64_t)now; break;
+      case SCHED_F_SUM_WAITING: v = sum_waiting; break;
+      default: break;
+    }
+    if (lane < SCHED_NF) P.out[(size_t)lane * P.n_reps + rep] = v;
+    if (TRACE && rep == 0 && lane == 0) *P.log_n = log_n;
+  }
+};
+
+template <int POL, bool TRACE>
+__global__ void __launch_bounds__(256) sim_kernel(const DevParams P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int wib = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int slot = blockIdx.x * (blockDim.x >> 5) + wib;
+  const size_t ring_base = (size_t)slot * P.n_rings * P.ring_cap;
+  WarpSim<POL, TRACE> sim(P, smem + (size_t)wib * P.warp_smem, lane, ring_base);
+  for (;;) {
+    uint32_t r = 0;
+    if (lane == 0) r = atomicAdd(P.work_counter, 1u);
+    r = __shfl_sync(FULL, r, 0);
+    if (r >= P.n_reps) break;
+    sim.run(r);
+  }
+}
+
+template <int POL, bool TRACE>
+cudaError_t launch_t(const DevParams& p, int grid, int block, size_t smem, cudaStream_t s) {
+  auto k = sim_kernel<POL, TRACE>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<grid, block, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int POL, bool TRACE>
+cudaError_t occ_t(int block, size_t smem, int* bps) {
+  auto k = sim_kernel<POL, TRACE>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k, block, smem);
+}
+
+template <int POL, bool TRACE>
+int regs_t() {
+  cudaFuncAttributes a;
+  if (cudaFuncGetAttributes(&a, sim_kernel<POL, TRACE>) != cudaSuccess) return -1;
+  return a.numRegs;
+}
+
+}  // namespace
+
+cudaError_t launch_sim(const DevParams& p, int grid, int block, size_t smem, cudaStream_t s) {
+  if (p.trace_mode) {
+    switch (p.policy) {
+      case SCHED_WAIT: return launch_t<SCHED_WAIT, true>(p, grid, block, smem, s);
+      case SCHED_NESTED: return launch_t<SCHED_NESTED, true>(p, grid, block, smem, s);
+      default: return launch_t<SCHED_FCFS, true>(p, grid, block, smem, s);
+    }
+  }
+  switch (p.policy) {
+    case SCHED_WAIT: return launch_t<SCHED_WAIT, false>(p, grid, block, smem, s);
+    case SCHED_NESTED: return launch_t<SCHED_NESTED, false>(p, grid, block, smem, s);
+    default: return launch_t<SCHED_FCFS, false>(p, grid, block, smem, s);
+  }
+}
+
+cudaError_t sim_occupancy(int policy, int trace, int block, size_t smem, int* bps) {
+  if (trace) {
+    switch (policy) {
+      case SCHED_WAIT: return occ_t<SCHED_WAIT, true>(block, smem, bps);
+      case SCHED_NESTED: return occ_t<SCHED_NESTED, true>(block, smem, bps);
+      default: return occ_t<SCHED_FCFS, true>(block, smem, bps);
+    }
+  }
+  switch (policy) {
+    case SCHED_WAIT: return occ_t<SCHED_WAIT, false>(block, smem, bps);
+    case SCHED_NESTED: return occ_t<SCHED_NESTED, false>(block, smem, bps);
+    default: return occ_t<SCHED_FCFS, false>(block, smem, bps);
+  }
+}
+
+int sim_regs_per_thread(int policy, int trace) {
+  if (trace) {
+    switch (policy) {
+      case SCHED_WAIT: return regs_t<SCHED_WAIT, true>();
+      case SCHED_NESTED: return regs_t<SCHED_NESTED, true>();
+      default: return regs_t<SCHED_FCFS, true>();
+    }
+  }
+  switch (policy) {
+    case SCHED_WAIT: return regs_t<SCHED_WAIT, false>();
+    case SCHED_NESTED: return regs_t<SCHED_NESTED, false>();
+    default: return regs_t<SCHED_FCFS, false>();
+  }
+}
+
+}  // namespace waitsim

@@ -1,0 +1,222 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle (-m gpu).
+
+Bar: every integer field of every per-replication row is
+bit-exact (counts, KV peaks, 128-bit tick sums, completion batch indices,
+the trajectory hash); batch logs of explicit traces are identical.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle
+import workloads as W
+from oracle import fluid as fl
+
+pytestmark = pytest.mark.gpu
+
+SEG3A = [20, 40, 80, 160]
+SEG10 = [50 * k for k in range(1, 11)]
+SEG4 = [100, 200, 300]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2504_11320_b200 import lib
+    lib()
+
+
+def gpu_rows(wl, pol, thr, n, horizon_s=None, rep_begin=0, seed=None, **kw):
+    from paper_2504_11320_b200 import Scheduler
+    s = Scheduler(wl, pol, None if pol.kind == W.FCFS else thr, **kw)
+    out = s.run_host(wl.seed if seed is None else seed, rep_begin, n,
+                     wl.horizon_s if horizon_s is None else horizon_s)
+    s.close()
+    return out
+
+
+def assert_rows_equal(got, ref, what=""):
+    assert got.shape == ref.shape
+    if not np.array_equal(got, ref):
+        bad = {oracle.FIELDS[f]: int(np.sum(got[f] != ref[f])) for f in range(ref.shape[0])
+               if not np.array_equal(got[f], ref[f])}
+        reps = sorted(set(np.nonzero((got != ref).any(axis=0))[0].tolist()))[:5]
+        st = got[oracle.F["status"], reps].tolist()
+        raise AssertionError(f"{what}: mismatching fields {bad}, first reps {reps}, gpu status {st}")
+
+
+def check(wl, pol, thr, n, horizon_s=None, **kw):
+    ref = oracle.run(wl, pol, thr, n_reps=n, n_threads=8, horizon_s=horizon_s)
+    got = gpu_rows(wl, pol, thr, n, horizon_s, **kw)
+    assert_rows_equal(got, ref, f"{wl.name}/{W.POLICY_NAMES[pol.kind]}")
+    assert (got[oracle.F["status"]] == 0).all()
+    return got
+
+
+# ----------------------------------------------------------- configs
+def test_c1_all_policies():
+    check(W.C1, W.Policy(W.WAIT), [1], 64)          # LIFO-eviction regime (M < M^pi)
+    check(W.C1P, W.Policy(W.WAIT), [1], 64)         # eviction-free
+    check(W.C1, W.Policy(W.FCFS, B=32), [0], 64)
+    check(W.C1, W.Policy(W.NESTED, seg_end=[16]), [1], 64)
+    check(W.C1, W.Policy(W.WAIT), [3], 32)
+
+
+def test_c2_wait_fluid_heuristic_fcfs():
+    check(W.C2, W.Policy(W.WAIT), fl.wait_fluid_integer(W.C2), 48, horizon_s=2.0)
+    check(W.C2, W.Policy(W.WAIT), fl.wait_heuristic(W.C2, 1024), 48, horizon_s=2.0)
+    check(W.C2, W.Policy(W.FCFS, B=1024), [0], 48, horizon_s=2.0)
+
+
+def test_c2_full_horizon_sample():
+    check(W.C2, W.Policy(W.WAIT), [16, 16], 16)
+    check(W.C2, W.Policy(W.FCFS, B=1024), [0], 16)
+
+
+def test_c3a_nested_strict_and_paper():
+    check(W.C3A, W.Policy(W.NESTED, seg_end=SEG3A), fl.nested_strict(W.C3A, SEG3A), 24, horizon_s=20.0)
+    check(W.C3A, W.Policy(W.NESTED, seg_end=SEG3A), W.PAPER_NESTED_RATIO_C3A, 24, horizon_s=20.0)
+    check(W.C3A, W.Policy(W.FCFS, B=1024), [0], 24, horizon_s=20.0)
+
+
+def test_c3b_geometric_marks():
+    check(W.C3B, W.Policy(W.NESTED, seg_end=SEG10), fl.nested_strict(W.C3B, SEG10), 16, horizon_s=20.0)
+    check(W.C3B, W.Policy(W.FCFS, B=2048), [0], 16, horizon_s=20.0)
+
+
+@pytest.mark.parametrize("i", range(5))
+def test_c4_rate_sweep(i):
+    wl = W.c4(i)
+    check(wl, W.Policy(W.WAIT), fl.wait_fluid_integer(wl), 12, horizon_s=8.0)
+    check(wl, W.Policy(W.NESTED, seg_end=SEG4), fl.nested_strict(wl, SEG4), 12, horizon_s=8.0)
+    check(wl, W.Policy(W.FCFS, B=1024), [0], 12, horizon_s=8.0)
+
+
+@pytest.mark.parametrize("qps", [55.0, 110.0])
+def test_c5_chat_shaped(qps):
+    wl = W.c5(qps)
+    kw = dict(max_resident=4096, restart_cap=1 << 16)
+    check(wl, W.Policy(W.NESTED, seg_end=SEG10), W.PAPER_NESTED_RATIO_C5, 8, horizon_s=120.0, **kw)
+    check(wl, W.Policy(W.FCFS, B=1024), [0], 8, horizon_s=120.0, **kw)
+
+
+# ------------------------------------------------- random small systems
+@pytest.mark.parametrize("seed", range(40))
+def test_random_small_workloads(seed):
+    rng = np.random.default_rng(1000 + seed)
+    wl = W.random_small(rng, horizon_s=1.5)
+    maxlp = max(v for t in wl.lp_tab for v, _ in t)
+    seg = sorted({int(x) for x in rng.integers(1, maxlp + 1, 2)} | {maxlp})
+    check(wl, W.Policy(W.WAIT), [int(rng.integers(1, 5)) for _ in range(wl.K)], 16)
+    check(wl, W.Policy(W.FCFS, B=int(rng.integers(1, 40)),
+                       tok_budget=int(rng.choice([0, 0, 12]))), [0], 16)
+    check(wl, W.Policy(W.NESTED, seg_end=seg),
+          sorted([int(x) for x in rng.integers(1, 5, len(seg))], reverse=True), 16)
+
+
+# --------------------------------------------------------- explicit traces
+def test_example2_trace_log():
+    from paper_2504_11320_b200 import Scheduler
+    from test_oracle import _ex2_trace
+    tr, t_end = _ex2_trace()
+    pol = W.Policy(W.FCFS, B=1000)
+    ref_rows, ref_log = oracle.run_trace(W.EX2, pol, [0], [tr], log_cap=32, horizon_s=t_end / 1e12)
+    s = Scheduler(W.EX2, pol)
+    rows, log = s.run_trace([tr], t_end / 1e12, log_cap=32)
+    assert np.array_equal(log, ref_log)
+    assert_rows_equal(rows, ref_rows, "EX2")
+
+
+def test_bruteforce_tiny_traces():
+    """P20(a): every multiset of <= 5 arrivals on a 5-point grid, M in 3..8,
+    l, l' in {1,2}, three policies: GPU rows == oracle rows."""
+    import itertools
+    from paper_2504_11320_b200 import Scheduler
+    unit = 4 * 10 ** 9
+    for l, lp in [(1, 1), (1, 2), (2, 1), (2, 2)]:
+        traces = []
+        for k in range(6):
+            for combo in itertools.combinations_with_replacement(range(5), k):
+                traces.append([(x * unit, 0, l, lp) for x in combo])
+        for M in range(l + lp, 9):
+            wl = W.Workload("bf", [1.0], [W.fixed(l)], [W.fixed(lp)], M=M, horizon_s=0.1,
+                            seed=0, d0_s=0.005, d1_s=0.001)
+            for pol, thr in [(W.Policy(W.FCFS, B=3), [0]), (W.Policy(W.WAIT), [1]),
+                             (W.Policy(W.WAIT), [2]), (W.Policy(W.NESTED, seg_end=[lp]), [2])]:
+                ref, _ = oracle.run_trace(wl, pol, thr, traces)
+                s = Scheduler(wl, pol, None if pol.kind == W.FCFS else thr)
+                got, _ = s.run_trace(traces, 0.1)
+                s.close()
+                assert_rows_equal(got, ref, f"bf l={l} lp={lp} M={M} pol={pol.kind}")
+
+
+def test_multiclass_traces_with_ties():
+    """Same-tick arrivals across classes, restarts and tiny M on 2-3 classes."""
+    from paper_2504_11320_b200 import Scheduler
+    rng = np.random.default_rng(7)
+    for trial in range(30):
+        K = int(rng.integers(2, 4))
+        l = [int(rng.integers(1, 4)) for _ in range(K)]
+        lp = [int(rng.integers(1, 5)) for _ in range(K)]
+        M = max(a + b for a, b in zip(l, lp)) + int(rng.integers(0, 8))
+        wl = W.Workload("mc", [1.0] * K, [W.fixed(x) for x in l], [W.fixed(x) for x in lp],
+                        M=M, horizon_s=0.2, seed=0, d0_s=0.003, d1_s=0.0005)
+        traces = []
+        for _ in range(8):
+            n = int(rng.integers(0, 25))
+            ts = sorted(int(x) * 2 * 10 ** 9 for x in rng.integers(0, 40, n))
+            cl = [int(x) for x in rng.integers(0, K, n)]
+            tr = sorted(zip(ts, cl), key=lambda x: (x[0], x[1]))
+            traces.append([(t, c, l[c], lp[c]) for t, c in tr])
+        maxlp = max(lp)
+        for pol, thr in [(W.Policy(W.FCFS, B=int(rng.integers(1, 10))), [0]),
+                         (W.Policy(W.WAIT), [int(rng.integers(1, 4)) for _ in range(K)]),
+                         (W.Policy(W.NESTED, seg_end=sorted({1, maxlp})), None)]:
+            if thr is None:
+                thr = sorted([int(x) for x in rng.integers(1, 4, len(pol.seg_end))], reverse=True)
+            ref, _ = oracle.run_trace(wl, pol, thr, traces)
+            s = Scheduler(wl, pol, None if pol.kind == W.FCFS else thr)
+            got, _ = s.run_trace(traces, 0.2)
+            s.close()
+            assert_rows_equal(got, ref, f"trial {trial} pol {pol.kind}")
+
+
+# ---------------------------------------------- sharding / determinism / errors
+def test_sharding_invariance_and_determinism():
+    pol, thr = W.Policy(W.WAIT), [16, 16]
+    full = gpu_rows(W.C2, pol, thr, 64, horizon_s=1.0)
+    again = gpu_rows(W.C2, pol, thr, 64, horizon_s=1.0)
+    assert np.array_equal(full, again)
+    for g in (2, 4, 8):
+        parts = [gpu_rows(W.C2, pol, thr, 64 // g, horizon_s=1.0, rep_begin=i * 64 // g) for i in range(g)]
+        assert np.array_equal(np.concatenate(parts, axis=1), full)
+
+
+def test_capacity_overflow_is_reported():
+    rows = gpu_rows(W.C2, W.Policy(W.FCFS, B=1024), [0], 4, horizon_s=1.0, max_resident=64)
+    assert (rows[oracle.F["status"]] == 1).all()
+
+
+def test_full_size_bench_config_sampled():
+    """C2 at the bench launch configuration (10^4 replications, both
+    policies), sampled replications checked against the oracle one by one."""
+    from paper_2504_11320_b200 import Scheduler
+    from paper_2504_11320_b200.sim import run_rows
+    idx = [0, 1, 777, 4095, 5000, 9998, 9999]
+    for pol, thr in [(W.Policy(W.WAIT), [16, 16]), (W.Policy(W.FCFS, B=1024), [0])]:
+        s = Scheduler(W.C2, pol, None if pol.kind == W.FCFS else thr)
+        rows = run_rows(s, W.C2.seed, 0, 10_000, W.C2.horizon_s)
+        torch.cuda.synchronize()
+        got = rows.cpu().numpy().view(np.uint64)
+        assert (got[oracle.F["status"]] == 0).all()
+        for i in idx:
+            ref = oracle.run(W.C2, pol, thr, n_reps=1, rep_begin=i)
+            assert_rows_equal(got[:, i:i + 1], ref, f"C2 rep {i}")
+        # properties at any size: conservation, memory bound
+        f = lambda k: got[oracle.F[k]].astype(object)
+        assert (f("arrivals") == f("completed") + f("completed_after_T") + f("final_waiting")
+                + f("final_resident")).all()
+        assert (got[oracle.F["max_kv_peak"]] <= W.C2.M).all()
+        s.close()

@@ -1,0 +1,3 @@
+set -x
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+tail -40 gpurun_out/pytest_gpu.log
