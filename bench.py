@@ -91,16 +91,22 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(wl, policies, reps, threads):
-    """The oracle as it stands on the host cores, bounded sample."""
+def cpu_baseline(wl, policies, reps, threads, min_wall=1.5, max_reps=1 << 15):
+    """The oracle as it stands on the host cores, on a bounded sample: the
+    replication count doubles until one pass takes >= min_wall seconds
+    (>= 10-30 s of CPU work on a multi-core host).  Returns (rate, wall,
+    request_steps, reps)."""
     import oracle
-    t0 = time.perf_counter()
-    steps = 0
-    for pol, thr in policies:
-        rows = oracle.run(wl, pol, thr, n_reps=reps, rep_begin=0, n_threads=threads)
-        steps += int(rows[oracle.F["request_steps"]].sum())
-    dt = time.perf_counter() - t0
-    return steps / dt, dt, steps
+    while True:
+        t0 = time.perf_counter()
+        steps = 0
+        for pol, thr in policies:
+            rows = oracle.run(wl, pol, thr, n_reps=reps, rep_begin=0, n_threads=threads)
+            steps += int(rows[oracle.F["request_steps"]].sum())
+        dt = time.perf_counter() - t0
+        if dt >= min_wall or reps >= max_reps:
+            return steps / dt, dt, steps, reps
+        reps *= 2
 
 
 def run_reference(args):
@@ -222,6 +228,8 @@ def main():
     total_b = int(sum(tot_int[i * nI + AGG_INT.index("batches")].item() for i in range(len(scheds))))
     total_c = int(sum(tot_int[i * nI + AGG_INT.index("completed")].item() for i in range(len(scheds))))
     bad = int(sum(tot_int[i * nI + AGG_INT.index("status")].item() for i in range(len(scheds))))
+    if bad:
+        raise SystemExit(f"{bad} replications reported a capacity status != 0: not a valid run")
     value = total_rs / elapsed
 
     # e2e: the same metric through the host-buffer C-ABI call (D2H inside)
@@ -288,10 +296,10 @@ def main():
         from oracle import fluid as fl
         threads = os.cpu_count() or 1
         pols = [(W2.Policy(W2.WAIT), fl.wait_fluid_integer(wl)), (W2.Policy(W2.FCFS, B=1024), [0])]
-        v, dt, n = cpu_baseline(wl, pols, args.cpu_reps, threads)
+        v, dt, n, nr = cpu_baseline(wl, pols, args.cpu_reps, threads)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
-                                "sample": f"C2 full horizon, {args.cpu_reps} replications x 2 policies "
-                                          f"({n} request-steps, {dt:.1f} s wall)"}
+                                "sample": f"C2 full horizon, {nr} replications x 2 policies "
+                                          f"({n} request-steps, {dt:.2f} s wall on {threads} threads)"}
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

@@ -129,16 +129,38 @@ __device__ __forceinline__ int64_t bcast64(int64_t v, int src) { return __shfl_s
 __device__ __forceinline__ uint32_t bcast32(uint32_t v, int src) { return __shfl_sync(FULL, v, src); }
 
 // ------------------------------------------------------------- the warp sim
+// resident record, packed: l | l' << 16 | s << 32 | meta << 48
+__device__ __forceinline__ uint64_t pack_q(uint32_t l, uint32_t lp, uint32_t s, uint32_t meta) {
+  return (uint64_t)l | ((uint64_t)lp << 16) | ((uint64_t)s << 32) | ((uint64_t)meta << 48);
+}
+constexpr uint32_t META_RESTART = 0x200;  // staging mark: came from a restart ring
+
+// # of leading entries of the sorted array v[0..n) that precede `key`
+// (v <= key if le, v < key otherwise)
+__device__ __forceinline__ uint32_t count_before(const int64_t* v, uint32_t n, int64_t key, bool le) {
+  uint32_t lo = 0, len = n;
+  while (len > 0) {
+    const uint32_t half = len >> 1;
+    const int64_t x = v[lo + half];
+    if (le ? (x <= key) : (x < key)) { lo += half + 1; len -= half + 1; } else { len = half; }
+  }
+  return lo;
+}
+
 template <int POL, bool TRACE>
 struct WarpSim {
   const DevParams& P;
   const int lane;
   // shared-memory views (this warp's slice)
-  int64_t* ra; uint16_t* rl; uint16_t* rlp; uint16_t* rs; uint16_t* rm;
+  int64_t* ra;                       // [Rc] arrival tick of each resident
+  uint64_t* rq;                      // [Rc] packed (l, l', s, meta)
   int64_t* vt;                       // [K][32] visibility windows
-  int64_t* at; uint16_t* al; uint16_t* alp;  // [K][32] admission windows
-  uint32_t* cnt;                     // [64]
-  uint32_t* rank;                    // [32]
+  int64_t* at;                       // [K][32] admission windows (t)
+  int64_t* re;                       // [32] staged restart-ring eviction ticks
+  uint16_t* al; uint16_t* alp;       // [K][32] admission windows (l, l')
+  uint32_t* cnt;                     // [64] WAIT: residents per class; NESTED: [k] / [32+k]
+  uint32_t* rank;                    // [32] NESTED per-segment rank cursors
+  uint32_t* snap;                    // [32] NESTED entry counts at decision time
   size_t ring_base;                  // first ring entry of this warp slot
 
   // per-class cursor state, lane c holds class c (and ring c for WAIT; ring 0
@@ -148,6 +170,7 @@ struct WarpSim {
   int64_t vprev, aprev;
   uint32_t sv_k, sv_rhead;           // saved admission cursor (drop/rewind)
   int64_t sv_prev;
+  uint32_t newc;                     // WAIT: admissions of class `lane` this epoch
 
   // replication
   uint32_t rep, rglob;
@@ -169,21 +192,23 @@ struct WarpSim {
       : P(p), lane(lane_), ring_base(rb) {
     const uint32_t Rc = p.Rc;
     ra = (int64_t*)base;
-    vt = ra + Rc;
+    rq = (uint64_t*)(ra + Rc);
+    vt = (int64_t*)(rq + Rc);
     at = vt + p.K * 32;
-    rl = (uint16_t*)(at + p.K * 32);
-    rlp = rl + Rc;
-    rs = rlp + Rc;
-    rm = rs + Rc;
-    al = rm + Rc;
+    re = at + p.K * 32;
+    al = (uint16_t*)(re + 32);
     alp = al + p.K * 32;
     cnt = (uint32_t*)(((uintptr_t)(alp + p.K * 32) + 15) & ~(uintptr_t)15);
     rank = cnt + 64;
+    snap = rank + 32;
   }
 
-  __device__ __forceinline__ int ring_of(int c) const { return POL == SCHED_WAIT ? c : 0; }
   __device__ __forceinline__ size_t ring_slot(int q, uint32_t pos) const {
     return ring_base + (size_t)q * P.ring_cap + (pos % P.ring_cap);
+  }
+  __device__ __forceinline__ uint32_t nested_key(uint32_t s) const {  // counter slot of stage s
+    const uint32_t info = __ldg(P.stage_info + s);
+    return (info & 0x7F) + ((info >> 7) ? 32u : 0u);
   }
 
   // ---------------------------------------------------- S1 arrival windows
@@ -232,16 +257,6 @@ struct WarpSim {
   __device__ __forceinline__ uint32_t kadm(int c) const { return bcast32(k_adm, c); }
   __device__ __forceinline__ uint32_t rcount(int q) const { return bcast32(rtail, q) - bcast32(rhead, q); }
 
-  // ensure class c's admission window holds arrival k_adm(c)
-  __device__ __forceinline__ void adm_window(int c) {
-    const uint32_t ka = kadm(c), ab = bcast32(abase, c);
-    if (ka == ab + 32) {
-      const int64_t carry = at[c * 32 + 31];
-      fill<true>(c, ka, carry, at, al, alp);
-      if (lane == c) { abase = ka; aprev = carry; }
-    }
-  }
-
   // ------------------------------------------------------ S2 ingestion
   // INGEST (DESIGN.md §4.4 step 1): arrivals with t <= now and t < T become
   // visible (join their FIFO).  Cursor only: count + arrival-time sum.
@@ -277,103 +292,133 @@ struct WarpSim {
     return best;
   }
 
-  __device__ __forceinline__ uint32_t waiting_class(int c) const {
-    return kvis(c) - kadm(c) + (POL == SCHED_WAIT ? rcount(c) : 0u);
-  }
   __device__ uint32_t waiting_total() const {
-    uint32_t w = 0;
-    for (int c = 0; c < P.K; ++c) w += kvis(c) - kadm(c);
-    const int nr = POL == SCHED_WAIT ? P.K : 1;
-    for (int q = 0; q < nr; ++q) w += rcount(q);
-    return w;
+    uint32_t w = lane < P.K ? k_vis - k_adm : 0u;
+    if (lane < (POL == SCHED_WAIT ? P.K : 1)) w += rtail - rhead;
+    return __reduce_add_sync(FULL, w);
   }
 
   // ------------------------------------------------------- admissions
-  // stage one prompt at resident slot n_res + n_new (prefill -> stage 1)
-  __device__ __forceinline__ bool stage_one(int64_t a, uint32_t l, uint32_t lp, uint16_t meta) {
-    const uint32_t i = n_res + n_new;
-    if (i >= P.Rc) { status = 1; return false; }
-    if (lane == 0) { ra[i] = a; rl[i] = (uint16_t)l; rlp[i] = (uint16_t)lp; rs[i] = 1; rm[i] = meta; }
-    __syncwarp();
-    ++n_new;
-    sum_new_l += l;
-    return true;
-  }
-  // take the arrival at the head of class c's cursor
-  __device__ __forceinline__ bool take_arrival(int c) {
-    adm_window(c);
-    const uint32_t j = kadm(c) - bcast32(abase, c);
-    const int64_t t = at[c * 32 + j];
-    const uint32_t l = al[c * 32 + j], lp = alp[c * 32 + j];
-    if (!stage_one(t, l, lp, (uint16_t)c)) return false;
-    if (lane == c) ++k_adm;
-    return true;
-  }
-  __device__ __forceinline__ bool take_restart(int q) {
-    const uint32_t h0 = bcast32(rhead, q);
-    const size_t e = ring_slot(q, h0);
-    const int64_t a = P.ring_a[e];
-    const uint32_t llp = P.ring_llp[e];
-    const uint16_t meta = (uint16_t)((POL == SCHED_WAIT ? q : 0) | ((llp >> 31) ? META_FT : 0));
-    if (!stage_one(a, llp & 0xFFFFu, (llp >> 16) & 0x7FFFu, meta)) return false;
-    if (lane == q) ++rhead;
-    return true;
-  }
-  // Which source holds the FIFO head?  Arrivals are ordered (t, class);
+  // Take up to `want` prompts from the head of FIFO q, in FIFO order, and
+  // stage them at resident slots n_res + n_new ... (prefill -> stage 1).
+  // WAIT: FIFO q = class q's arrivals + restart ring q; otherwise one FIFO
+  // = all classes' arrivals + ring 0.  FIFO order: arrivals by (t, class);
   // a restart evicted at tick e precedes exactly the arrivals with t > e
-  // (restarts join the tail after same-tick arrivals).
-  // Returns class index, 32 for the restart ring, -1 if empty.
-  __device__ int head_source_merged(int64_t* l_out) {
-    int best = -1;
-    int64_t bt = TMAX;
-    for (int c = 0; c < P.K; ++c) {
-      if (kadm(c) < kvis(c)) {
-        adm_window(c);
-        const int64_t t = at[c * 32 + (kadm(c) - bcast32(abase, c))];
-        if (t < bt) { bt = t; best = c; }
+  // (DESIGN.md §4.4).  Lane-parallel: each candidate's FIFO rank is the
+  // number of candidates before it (binary searches over the other sources'
+  // windows); FCFS additionally cuts at the first prompt failing the
+  // admission test (reading R15).
+  template <bool FCFS_COND>
+  __device__ bool take_fifo(int q, uint32_t want) {
+    const int c_lo = POL == SCHED_WAIT ? q : 0;
+    const int c_hi = POL == SCHED_WAIT ? q + 1 : P.K;
+    while (want > 0) {
+      // (1) align class windows so each holds min(pending, 32) from k_adm
+      uint32_t my_j = 0, my_n = 0, total = 0;
+      for (int c = c_lo; c < c_hi; ++c) {
+        const uint32_t ka = kadm(c);
+        const uint32_t p = kvis(c) - ka;
+        if (p == 0) continue;
+        uint32_t j = ka - bcast32(abase, c);
+        if (j == 32 || (j > 0 && p > 32 - j)) {
+          const int64_t prev = j > 0 ? at[c * 32 + j - 1] : bcast64(aprev, c);
+          fill<true>(c, ka, prev, at, al, alp);
+          if (lane == c) { abase = ka; aprev = prev; }
+          j = 0;
+        }
+        const uint32_t n = min(p, 32u - j);
+        if (lane == c) { my_j = j; my_n = n; }
+        total += n;
       }
-    }
-    if (rcount(0) > 0) {
-      const size_t e = ring_slot(0, bcast32(rhead, 0));
-      if (best < 0 || P.ring_e[e] < bt) {
-        if (l_out) *l_out = P.ring_llp[e] & 0xFFFFu;
-        return 32;
+      const uint32_t nr = min(rcount(q), 32u);
+      const uint32_t h0 = bcast32(rhead, q);
+      if (nr > 0) {
+        __syncwarp();
+        if ((uint32_t)lane < nr) re[lane] = P.ring_e[ring_slot(q, h0 + lane)];
+        __syncwarp();
       }
-    }
-    if (best >= 0 && l_out) *l_out = al[best * 32 + (kadm(best) - bcast32(abase, best))];
-    return best;
-  }
-  __device__ int head_source_class(int c) {
-    const bool arr = kadm(c) < kvis(c);
-    int64_t t = TMAX;
-    if (arr) { adm_window(c); t = at[c * 32 + (kadm(c) - bcast32(abase, c))]; }
-    if (rcount(c) > 0 && (!arr || P.ring_e[ring_slot(c, bcast32(rhead, c))] < t)) return 32;
-    return arr ? c : -1;
-  }
-
-  // bulk take of `cnt_` arrivals of class c (no restarts pending): lane-parallel
-  __device__ bool take_bulk(int c, uint32_t cnt_) {
-    while (cnt_ > 0) {
-      adm_window(c);
-      const uint32_t j = kadm(c) - bcast32(abase, c);
-      const uint32_t take = min(cnt_, 32u - j);
-      if (n_res + n_new + take > P.Rc) { status = 1; return false; }
-      const bool act = (uint32_t)lane < take;
-      uint32_t l = 0;
-      if (act) {
-        const uint32_t d = n_res + n_new + lane;
-        l = al[c * 32 + j + lane];
-        ra[d] = at[c * 32 + j + lane];
-        rl[d] = (uint16_t)l;
-        rlp[d] = alp[c * 32 + j + lane];
-        rs[d] = 1;
-        rm[d] = (uint16_t)c;
+      const uint32_t ncand = total + nr;
+      if (ncand == 0) break;
+      const uint32_t base = n_res + n_new;
+      // stage at most what can be taken: `want` (WAIT/NESTED) or the B bound (FCFS)
+      uint32_t m = min(min(ncand, 32u), want);
+      if (FCFS_COND) m = min(m, P.B > base ? P.B - base : 0u);
+      if (m == 0) break;
+      if (base + m > P.Rc) { status = 1; return false; }
+      // (2) rank candidates; rank < m -> staged at slot base + rank
+      for (uint32_t g0 = 0; g0 < ncand; g0 += 32) {
+        const uint32_t g = g0 + lane;
+        const bool act = g < ncand;
+        int src = 32;
+        uint32_t pos = 0, acc = 0;
+        for (int c = c_lo; c < c_hi; ++c) {
+          const uint32_t n = bcast32(my_n, c);
+          if (src == 32 && g >= acc && g < acc + n) { src = c; pos = g - acc; }
+          acc += n;
+        }
+        if (src == 32) pos = g - acc;
+        const uint32_t jsrc = __shfl_sync(FULL, my_j, src & 31);
+        int64_t key = 0, a = 0;
+        uint32_t l = 0, lp = 0, meta = 0, r = pos;
+        if (act) {
+          if (src < 32) {
+            const int idx = src * 32 + (int)(jsrc + pos);
+            key = at[idx]; a = key; l = al[idx]; lp = alp[idx]; meta = (uint32_t)src;
+            r += count_before(re, nr, key, false);       // restarts with e < t
+          } else {
+            key = re[pos];
+            const size_t e = ring_slot(q, h0 + pos);
+            a = P.ring_a[e];
+            const uint32_t llp = P.ring_llp[e];
+            l = llp & 0xFFFFu; lp = (llp >> 16) & 0x7FFFu;
+            meta = (POL == SCHED_WAIT ? (uint32_t)q : 0u) | ((llp >> 31) ? META_FT : 0u) | META_RESTART;
+          }
+        }
+        for (int c = c_lo; c < c_hi; ++c) {
+          const uint32_t n = bcast32(my_n, c);
+          if (n == 0) continue;
+          const uint32_t jj = bcast32(my_j, c);
+          if (act && c != src)  // arrivals of class c before this candidate
+            r += count_before(at + c * 32 + jj, n, key, src == 32 || c < src);
+        }
+        if (act && r < m) {
+          ra[base + r] = a;
+          rq[base + r] = pack_q(l, lp, 1, meta);
+        }
       }
       __syncwarp();
-      sum_new_l += __reduce_add_sync(FULL, l);
+      // (3) how many to take
+      uint64_t qv = 0;
+      uint32_t l = 0;
+      if ((uint32_t)lane < m) { qv = rq[base + lane]; l = (uint32_t)(qv & 0xFFFF); }
+      uint32_t take;
+      if (FCFS_COND) {
+        const uint32_t pre = warp_incl_scan_u32(l, lane);
+        const bool ok = (uint32_t)lane < m && (n_res + n_new + lane < P.B) &&
+                        (KV + sum_new_l + (int64_t)pre <= P.M) &&
+                        (P.tok_budget == 0 || sum_new_l + (int64_t)pre <= (int64_t)P.tok_budget);
+        const uint32_t okm = __ballot_sync(FULL, ok);  // ok lanes form a prefix
+        take = okm == FULL ? 32u : (uint32_t)__ffs(~okm) - 1;
+      } else {
+        take = min(m, want);
+      }
+      if (take == 0) break;
+      // (4) consume: advance each source's cursor by what it contributed
+      const bool tk = (uint32_t)lane < take;
+      const uint32_t meta = (uint32_t)(qv >> 48);
+      const bool rst = tk && (meta & META_RESTART);
+      for (int c = c_lo; c < c_hi; ++c) {
+        const uint32_t cc = __popc(__ballot_sync(FULL, tk && !(meta & META_RESTART) && (meta & 0xFF) == (uint32_t)c));
+        if (lane == c) { k_adm += cc; newc += cc; }
+      }
+      const uint32_t crs = __popc(__ballot_sync(FULL, rst));
+      if (lane == q) { rhead += crs; if (POL == SCHED_WAIT) newc += crs; }
+      if (rst) rq[base + lane] = qv & ~((uint64_t)META_RESTART << 48);
       n_new += take;
-      if (lane == c) k_adm += take;
-      cnt_ -= take;
+      sum_new_l += __reduce_add_sync(FULL, tk ? l : 0u);
+      want -= take;
+      __syncwarp();
+      if (take < m) break;
     }
     return true;
   }
@@ -382,11 +427,10 @@ struct WarpSim {
   __device__ void save_cursors() {
     sv_k = k_adm;
     sv_rhead = rhead;
-    const uint32_t j = k_adm - abase;  // lane-local (own class)
     sv_prev = aprev;
-    // tick of arrival k_adm-1: window entry j-1 if j > 0 (read by every lane
-    // of its own class slot; lanes >= K hold garbage and never use it)
+    const uint32_t j = k_adm - abase;  // lane-local (own class)
     if (lane < P.K && j > 0 && j <= 32) sv_prev = at[lane * 32 + j - 1];
+    newc = 0;
   }
   __device__ void restore_cursors() {
     for (int c = 0; c < P.K; ++c) {
@@ -400,74 +444,16 @@ struct WarpSim {
       if (lane == c) k_adm = k;
     }
     rhead = sv_rhead;
+    newc = 0;
   }
 
   // ---------------------------------------------------- S3 decide + take
-  // Returns false for "no batch".  limit = max number of new admissions
-  // (used when re-taking after a drop).
   __device__ bool take_wait(uint32_t limit) {
     for (int c = 0; c < P.K && limit > 0; ++c) {
       if (!((Qmask >> c) & 1u)) continue;
-      uint32_t want = min(P.thr[c], limit);
+      const uint32_t want = min(P.thr[c], limit);
       limit -= want;
-      if (rcount(c) == 0) {
-        if (!take_bulk(c, want)) return false;
-      } else {
-        while (want-- > 0) {
-          const int src = head_source_class(c);
-          if (!(src == 32 ? take_restart(c) : take_arrival(c))) return false;
-        }
-      }
-    }
-    return true;
-  }
-  __device__ bool take_merged_n(uint32_t want) {
-    if (P.K == 1 && rcount(0) == 0) return take_bulk(0, want);
-    while (want-- > 0) {
-      const int src = head_source_merged(nullptr);
-      if (!(src == 32 ? take_restart(0) : take_arrival(src))) return false;
-    }
-    return true;
-  }
-  __device__ bool take_fcfs() {
-    if (P.K == 1 && rcount(0) == 0) {
-      // lane-parallel admission scan over the cursor window
-      for (;;) {
-        const uint32_t avail_all = kvis(0) - kadm(0);
-        if (avail_all == 0) break;
-        adm_window(0);
-        const uint32_t j = kadm(0) - bcast32(abase, 0);
-        const uint32_t avail = min(avail_all, 32u - j);
-        const bool act = (uint32_t)lane < avail;
-        const uint32_t l = act ? al[j + lane] : 0u;
-        const uint32_t pre = warp_incl_scan_u32(l, lane);
-        const bool ok = act && (n_res + n_new + lane < P.B) &&
-                        (KV + sum_new_l + (int64_t)pre <= P.M) &&
-                        (P.tok_budget == 0 || sum_new_l + (int64_t)pre <= (int64_t)P.tok_budget);
-        const uint32_t okm = __ballot_sync(FULL, ok);
-        const uint32_t take = okm == FULL ? 32u : (uint32_t)__ffs(~okm) - 1;  // ok lanes: a prefix
-        if (take == 0) break;
-        if (n_res + n_new + take > P.Rc) { status = 1; return false; }
-        if ((uint32_t)lane < take) {
-          const uint32_t d = n_res + n_new + lane;
-          ra[d] = at[j + lane]; rl[d] = (uint16_t)l; rlp[d] = alp[j + lane]; rs[d] = 1; rm[d] = 0;
-        }
-        __syncwarp();
-        sum_new_l += __shfl_sync(FULL, pre, take - 1);
-        n_new += take;
-        if (lane == 0) k_adm += take;
-        if (take < avail) break;
-      }
-      return true;
-    }
-    for (;;) {
-      if (n_res + n_new >= P.B) break;
-      int64_t l = 0;
-      const int src = head_source_merged(&l);
-      if (src < 0) break;
-      if (KV + sum_new_l + l > P.M) break;
-      if (P.tok_budget != 0 && sum_new_l + l > (int64_t)P.tok_budget) break;
-      if (!(src == 32 ? take_restart(0) : take_arrival(src))) return false;
+      if (!take_fifo<false>(c, want)) return false;
     }
     return true;
   }
@@ -478,12 +464,12 @@ struct WarpSim {
     if (POL == SCHED_WAIT) {
       // Algorithm 1: type j joins the batch iff n_j0 >= n_j;
       // all residents of qualifying types ride along (line 1490, invariant P14)
-      uint32_t q = 0, npr = 0;
+      uint32_t qq = 0, npr = 0;
       if (lane < P.K) {
         const uint32_t w = k_vis - k_adm + (rtail - rhead);
-        if (w >= P.thr[lane]) { q = 1; npr = cnt[lane]; }
+        if (w >= P.thr[lane]) { qq = 1; npr = cnt[lane]; }
       }
-      Qmask = __ballot_sync(FULL, q);
+      Qmask = __ballot_sync(FULL, qq);
       if (!Qmask) return false;
       n_plan_res = __reduce_add_sync(FULL, npr);
       save_cursors();
@@ -492,10 +478,9 @@ struct WarpSim {
       // Algorithm 2: largest k with Q_{k',entry} >= n_k' for all k' <= k
       // (PAPER.md:1640); batch min{n_k, Q_{k,s}} per stage (line 1642)
       if (waiting_total() < P.thr[0]) return false;
-      int ks = 0;
-      for (int k = 1; k < P.n_seg; ++k) {
-        if (cnt[32 + k] >= P.thr[k]) ks = k; else break;
-      }
+      const bool pass = lane >= 1 && lane < P.n_seg && cnt[32 + lane] >= P.thr[lane];
+      const uint32_t fail = ~__ballot_sync(FULL, pass) & ~1u;  // bit 0 = segment 1 (passed)
+      const int ks = min(__ffs(fail) - 2, P.n_seg - 1);
       kstar = ks;
       uint32_t npr = 0;
       if (lane <= ks) {
@@ -504,20 +489,13 @@ struct WarpSim {
       }
       n_plan_res = __reduce_add_sync(FULL, npr);
       save_cursors();
-      return take_merged_n(P.thr[0]);
+      return take_fifo<false>(0, P.thr[0]);
     } else {
       // FCFS new-first (R15)
       n_plan_res = n_res;
-      if (!take_fcfs()) return false;
+      if (!take_fifo<true>(0, 0xFFFFFFFFu)) return false;
       return n_res + n_new > 0;
     }
-  }
-
-  // membership of resident i (chunk-parallel), NESTED rank bookkeeping in
-  // rank[] (head order) -- only valid inside execute()
-  __device__ __forceinline__ bool in_plan_simple(uint16_t meta) const {
-    if (POL == SCHED_FCFS) return true;
-    return (Qmask >> (meta & 0xFF)) & 1u;
   }
 
   // --------------------------------------- S4 memory check / LIFO eviction
@@ -526,28 +504,29 @@ struct WarpSim {
     if (peak <= P.M) return;
     int64_t excess = peak - P.M;
     const uint32_t old_n = n_res;
-    if (POL == SCHED_NESTED) { if (lane < 32) rank[lane] = 0; __syncwarp(); }
+    if (POL == SCHED_NESTED) { rank[lane] = 0; snap[lane] = cnt[32 + lane]; __syncwarp(); }
     while (excess > 0 && n_res > 0) {
       const int idx = (int)n_res - 1 - lane;  // lane 0 = last admitted
       const bool valid = idx >= 0;
-      uint32_t l = 0, lp = 0, s = 0, meta = 0;
+      uint64_t qv = 0;
       int64_t a = 0;
-      if (valid) { l = rl[idx]; lp = rlp[idx]; s = rs[idx]; meta = rm[idx]; a = ra[idx]; }
-      uint32_t inp = 0;
-      if (valid) {
-        if (POL != SCHED_NESTED) inp = in_plan_simple((uint16_t)meta);
-      }
+      if (valid) { qv = rq[idx]; a = ra[idx]; }
+      const uint32_t l = (uint32_t)(qv & 0xFFFF), lp = (uint32_t)((qv >> 16) & 0xFFFF);
+      const uint32_t s = (uint32_t)((qv >> 32) & 0xFFFF), meta = (uint32_t)(qv >> 48);
+      uint32_t inp = 0, nkey = 0;
+      if (POL == SCHED_FCFS) inp = valid;
+      if (POL == SCHED_WAIT) inp = valid && ((Qmask >> (meta & 0xFF)) & 1u);
       if (POL == SCHED_NESTED) {
         const uint32_t info = valid ? __ldg(P.stage_info + s) : 0u;
         const int seg = info & 0x7F;
+        nkey = (info & 0x7F) + ((info >> 7) ? 32u : 0u);
         const bool entry = valid && (info >> 7) && seg <= kstar;
         const uint32_t key = entry ? s : (0x10000u + lane);
         const uint32_t grp = __match_any_sync(FULL, key);
         if (valid && seg <= kstar) {
           if (entry) {
             const uint32_t after = rank[seg] + __popc(grp & lanemask_lt());
-            const uint32_t r = cnt[32 + seg] - 1 - after;  // rank from the head
-            inp = r < P.thr[seg];
+            inp = snap[seg] - 1 - after < P.thr[seg];  // rank from the head
           } else {
             inp = 1;
           }
@@ -575,12 +554,13 @@ struct WarpSim {
         P.ring_a[e] = a;
         P.ring_e[e] = now;
         P.ring_llp[e] = l | (lp << 16) | ((meta & META_FT) ? 0x80000000u : 0u);
+        if (POL == SCHED_WAIT) atomicSub(&cnt[meta & 0xFF], 1u);
+        if (POL == SCHED_NESTED) atomicSub(&cnt[nkey], 1u);
       }
-      // advance ring tails (lane q owns ring q)
-      if (POL == SCHED_WAIT) {
+      if (POL == SCHED_WAIT) {  // advance ring tails (lane q owns ring q)
         for (int c = 0; c < P.K; ++c) {
-          const uint32_t m = __ballot_sync(FULL, ev && q == c);
-          if (lane == c) rtail += __popc(m);
+          const uint32_t mm = __ballot_sync(FULL, ev && q == c);
+          if (lane == c) rtail += __popc(mm);
         }
       } else if (lane == 0) {
         rtail += ne;
@@ -591,40 +571,39 @@ struct WarpSim {
       n_res -= ne;
       evictions += ne;
       n_evict += ne;
+      __syncwarp();
     }
     // close the gap between the surviving residents and the staged admissions
     if (n_res != old_n && n_new > 0) {
       for (uint32_t o = 0; o < n_new; o += 32) {
         const uint32_t i = o + lane;
-        int64_t a = 0; uint16_t l = 0, lp = 0, s = 0, m = 0;
-        if (i < n_new) { a = ra[old_n + i]; l = rl[old_n + i]; lp = rlp[old_n + i]; s = rs[old_n + i]; m = rm[old_n + i]; }
+        int64_t a = 0;
+        uint64_t qv = 0;
+        if (i < n_new) { a = ra[old_n + i]; qv = rq[old_n + i]; }
         __syncwarp();
-        if (i < n_new) { ra[n_res + i] = a; rl[n_res + i] = l; rlp[n_res + i] = lp; rs[n_res + i] = s; rm[n_res + i] = m; }
+        if (i < n_new) { ra[n_res + i] = a; rq[n_res + i] = qv; }
         __syncwarp();
       }
     }
     if (excess > 0) {
       // no residents left: drop the latest new admissions (they stay queued)
       uint32_t keep = n_new;
-      while (excess > 0 && keep > 0) { excess -= rl[n_res + keep - 1]; --keep; }
+      while (excess > 0 && keep > 0) { excess -= (int64_t)(rq[n_res + keep - 1] & 0xFFFF); --keep; }
       restore_cursors();
       n_new = 0;
       sum_new_l = 0;
       if (POL == SCHED_WAIT) take_wait(keep);
-      else take_merged_n(keep);  // FCFS never reaches here (admission bound)
+      else take_fifo<false>(0, keep);  // FCFS never gets here (admission bound)
     }
     peak = P.M + excess;
   }
 
   // ------------------------------------------------------ S5 execute
   // One pass over residents (+ the staged admissions) in admission order:
-  // per-member update, completions, compaction and counter recount.
+  // per-member update, completions, compaction; counters updated in place.
   __device__ void execute(uint32_t n_evict, int64_t peak, uint32_t waiting) {
     const uint32_t n_tot = n_res + n_new;
-    if (POL != SCHED_FCFS) {
-      if (lane < 32) { cnt[lane] = 0; cnt[32 + lane] = 0; rank[lane] = 0; }
-      __syncwarp();
-    }
+    if (POL == SCHED_NESTED) { rank[lane] = 0; __syncwarp(); }
     uint32_t tok = 0, n_done = 0, done_tok = 0, n_ft = 0, kv_free = 0, grow = 0;
     uint64_t done_a = 0, ft_a = 0;
     uint32_t wp = 0;
@@ -633,12 +612,17 @@ struct WarpSim {
       const bool valid = i < n_tot;
       const bool fresh = i >= n_res;
       int64_t a = 0;
-      uint32_t l = 0, lp = 0, s = 0, meta = 0;
-      if (valid) { a = ra[i]; l = rl[i]; lp = rlp[i]; s = rs[i]; meta = rm[i]; }
+      uint64_t qv = 0;
+      if (valid) { a = ra[i]; qv = rq[i]; }
+      const uint32_t l = (uint32_t)(qv & 0xFFFF), lp = (uint32_t)((qv >> 16) & 0xFFFF);
+      const uint32_t s = (uint32_t)((qv >> 32) & 0xFFFF);
+      uint32_t meta = (uint32_t)(qv >> 48);
       bool inp = false;
+      uint32_t key_s = 0;
       if (POL == SCHED_NESTED) {
         const uint32_t info = (valid && !fresh) ? __ldg(P.stage_info + s) : 0x7Fu;
         const int seg = info & 0x7F;
+        key_s = (info & 0x7F) + ((info >> 7) ? 32u : 0u);
         const bool act = valid && !fresh && seg <= kstar;
         const bool entry = act && (info >> 7);
         const uint32_t key = entry ? s : (0x10000u + lane);
@@ -646,8 +630,10 @@ struct WarpSim {
         if (act) inp = entry ? (rank[seg] + __popc(grp & lanemask_lt()) < P.thr[seg]) : true;
         __syncwarp();
         if (entry && (grp & lanemask_lt()) == 0) rank[seg] += __popc(grp);
+      } else if (POL == SCHED_WAIT) {
+        inp = valid && !fresh && ((Qmask >> (meta & 0xFF)) & 1u);
       } else {
-        inp = valid && !fresh && in_plan_simple((uint16_t)meta);
+        inp = valid && !fresh;
       }
       bool keep = valid;
       uint32_t ns = s;
@@ -662,33 +648,29 @@ struct WarpSim {
           ++n_done;
           done_tok += lp;
           done_a += (uint64_t)a;
+          if (POL == SCHED_WAIT) atomicSub(&cnt[meta & 0xFF], 1u);
+          if (POL == SCHED_NESTED) atomicSub(&cnt[key_s], 1u);
         } else {
           ns = s + 1;
           ++grow;
+          if (POL == SCHED_NESTED) {
+            const uint32_t key_n = nested_key(ns);
+            if (key_n != key_s) { atomicSub(&cnt[key_s], 1u); atomicAdd(&cnt[key_n], 1u); }
+          }
         }
       }
       const uint32_t km = __ballot_sync(FULL, keep);
       const uint32_t d = wp + __popc(km & lanemask_lt());
       __syncwarp();
       if (keep) {
-        if (d != i) { ra[d] = a; rl[d] = (uint16_t)l; rlp[d] = (uint16_t)lp; }
-        rs[d] = (uint16_t)ns;
-        rm[d] = (uint16_t)meta;
-      }
-      if (POL != SCHED_FCFS) {
-        uint32_t key;
-        if (POL == SCHED_WAIT) {
-          key = keep ? (meta & 0xFF) : (0x100u + lane);
-        } else {
-          const uint32_t info = keep ? __ldg(P.stage_info + ns) : 0u;
-          key = keep ? ((info & 0x7F) + ((info >> 7) ? 32u : 0u)) : (0x100u + lane);
-        }
-        const uint32_t grp = __match_any_sync(FULL, key);
-        if (keep && (grp & lanemask_lt()) == 0) cnt[key] += __popc(grp);
+        if (d != i) { ra[d] = a; rq[d] = pack_q(l, lp, ns, meta); }
+        else if (inp) rq[d] = pack_q(l, lp, ns, meta);
       }
       wp += __popc(km);
       __syncwarp();
     }
+    if (POL == SCHED_WAIT) { if (lane < P.K) cnt[lane] += newc; }
+    if (POL == SCHED_NESTED) { if (lane == 0) cnt[0] += n_new; }  // stage 1 = segment 1, non-entry
     // warp-uniform batch totals
     tok = __reduce_add_sync(FULL, tok);
     const uint32_t nd = __reduce_add_sync(FULL, n_done);
@@ -731,25 +713,7 @@ struct WarpSim {
     n_res = wp;
     n_new = 0;
     now = t_end;
-  }
-
-  // counters after an epoch whose plan emptied (evictions but no batch)
-  __device__ void recount() {
-    if (POL == SCHED_FCFS) return;
-    if (lane < 32) { cnt[lane] = 0; cnt[32 + lane] = 0; }
     __syncwarp();
-    for (uint32_t base = 0; base < n_res; base += 32) {
-      const uint32_t i = base + lane;
-      const bool valid = i < n_res;
-      uint32_t key = 0x100u + lane;
-      if (valid) {
-        if (POL == SCHED_WAIT) key = rm[i] & 0xFF;
-        else { const uint32_t info = __ldg(P.stage_info + rs[i]); key = (info & 0x7F) + ((info >> 7) ? 32u : 0u); }
-      }
-      const uint32_t grp = __match_any_sync(FULL, key);
-      if (valid && (grp & lanemask_lt()) == 0) cnt[key] += __popc(grp);
-      __syncwarp();
-    }
   }
 
   // ------------------------------------------------------------ run
@@ -766,14 +730,14 @@ struct WarpSim {
     log_n = 0;
     k_vis = vbase = k_adm = abase = rhead = rtail = 0;
     vprev = aprev = 0;
+    newc = 0;
     for (int c = 0; c < P.K; ++c) {
       fill<false>(c, 0, 0, vt, nullptr, nullptr);
       fill<true>(c, 0, 0, at, al, alp);
     }
-    if (POL != SCHED_FCFS) {
-      if (lane < 32) { cnt[lane] = 0; cnt[32 + lane] = 0; }
-      __syncwarp();
-    }
+    cnt[lane] = 0;
+    cnt[32 + lane] = 0;
+    __syncwarp();
     for (;;) {
       ingest();
       if (now >= P.T_t) break;                     // STOP
@@ -785,7 +749,7 @@ struct WarpSim {
       if (go) {
         memory(n_evict, peak);
         if (status) break;
-        if (n_plan_res + n_new == 0) { go = false; recount(); }
+        if (n_plan_res + n_new == 0) go = false;    // empty after eviction: wait (R27)
       }
       if (!go) {
         const int64_t nt = next_arrival();
