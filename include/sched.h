@@ -103,8 +103,8 @@ typedef struct {
 } sched_config;
 
 /* Validate and copy *cfg (every array is copied; cfg may be freed after),
- * convert times to ticks, build integer CDF tables and upload the class /
- * policy tables to `device`.  Errors: SCHED_E_INVALID (K = 0 or > 32,
+ * convert times to ticks and build integer CDF tables (host only: the tables
+ * are uploaded to `device` by the first sched_run / sched_run_trace).  Errors: SCHED_E_INVALID (K = 0 or > 32,
  * lambda < 0, l < 1, l' < 1, empty / zero-weight table, d0 <= 0, d1 < 0,
  * M < 1, bad thresholds / seg_end, B = 0 for FCFS), SCHED_E_UNSATISFIABLE
  * (some l + l' > M), SCHED_E_CUDA. */
