@@ -99,6 +99,9 @@ typedef struct {
   uint32_t tok_budget;        /* FCFS: max prefill tokens per iteration (0 = none) */
   uint32_t max_resident;      /* per-replication resident capacity (0 = derive) */
   uint32_t restart_cap;       /* per-FIFO restart ring capacity (0 = default 8192) */
+  uint32_t spec_resident;     /* speculative capacity of the main launch (0 = derive);
+                                 replications exceeding it are re-run with the safe
+                                 capacity by a fallback launch on the same stream */
   int32_t device;             /* CUDA device ordinal */
 } sched_config;
 
@@ -166,7 +169,9 @@ int sched_run_trace(sched_t h, const int64_t* t_ticks, const int32_t* cls,
 /* Launch configuration used by sched_run (for roofline accounting). */
 typedef struct {
   int32_t grid, block, warps_per_block, shared_bytes, blocks_per_sm, sm_count;
-  int32_t max_resident, restart_cap;
+  int32_t max_resident, restart_cap;      /* safe capacity, ring capacity */
+  int32_t spec_resident;                  /* main-launch capacity (== max_resident: no fallback) */
+  int32_t fallback_grid, fallback_warps_per_block;
 } sched_launch_info;
 int sched_get_launch_info(sched_t h, sched_launch_info* out);
 

@@ -51,7 +51,7 @@ class SchedConfig(C.Structure):
         ("policy", C.c_int32), ("n_thr", C.c_uint32), ("thresholds", C.POINTER(C.c_uint32)),
         ("n_seg", C.c_uint32), ("seg_end", C.POINTER(C.c_uint16)),
         ("B", C.c_uint32), ("tok_budget", C.c_uint32), ("max_resident", C.c_uint32),
-        ("restart_cap", C.c_uint32), ("device", C.c_int32),
+        ("restart_cap", C.c_uint32), ("spec_resident", C.c_uint32), ("device", C.c_int32),
     ]
 
 
@@ -71,7 +71,8 @@ class ThresholdReport(C.Structure):
 class LaunchInfo(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("grid", "block", "warps_per_block", "shared_bytes",
                                           "blocks_per_sm", "sm_count", "max_resident",
-                                          "restart_cap")]
+                                          "restart_cap", "spec_resident", "fallback_grid",
+                                          "fallback_warps_per_block")]
 
 
 _lib = None
@@ -122,7 +123,8 @@ class Scheduler:
     """
 
     def __init__(self, workload, policy, thresholds: Optional[Sequence[int]] = None,
-                 device: int = 0, max_resident: int = 0, restart_cap: int = 0):
+                 device: int = 0, max_resident: int = 0, restart_cap: int = 0,
+                 spec_resident: int = 0):
         keep = []
         cfg = SchedConfig()
 
@@ -159,15 +161,19 @@ class Scheduler:
         cfg.seg_end, cfg.n_seg = p, len(seg)
         cfg.B, cfg.tok_budget = policy.B, policy.tok_budget
         cfg.max_resident, cfg.restart_cap, cfg.device = max_resident, restart_cap, device
+        cfg.spec_resident = spec_resident
         h = C.c_void_p()
         _check(lib().sched_create(C.byref(h), C.byref(cfg)))
         self._h = h
         self.workload, self.policy, self.device = workload, policy, device
 
     def close(self):
-        if getattr(self, "_h", None):
-            lib().sched_destroy(self._h)
-            self._h = None
+        if getattr(self, "_h", None) and _lib is not None:
+            try:
+                _lib.sched_destroy(self._h)
+            except Exception:  # interpreter shutdown
+                pass
+        self._h = None
 
     __del__ = close
 

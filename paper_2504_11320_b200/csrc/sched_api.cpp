@@ -35,7 +35,7 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 struct sched_s {
   SetupInput in;
-  uint32_t tok_budget = 0, max_resident_cfg = 0, ring_cap = 8192;
+  uint32_t tok_budget = 0, max_resident_cfg = 0, spec_resident_cfg = 0, ring_cap = 8192;
   int device = 0;
   int64_t d0_t = 0, d1_t = 0;
   uint32_t max_lp = 0, min_l = 0;
@@ -55,9 +55,15 @@ struct sched_s {
   uint32_t* d_counter = nullptr;
   uint64_t* d_out = nullptr;
   size_t out_cap = 0;
-  // launch
+  // launch: main (speculative capacity Rc) and fallback (safe capacity Rc_safe)
   int grid = 0, block = 0, wpb = 0, blocks_per_sm = 0, sm_count = 0;
   uint32_t Rc = 0, warp_smem = 0;
+  int fb_grid = 0, fb_block = 0, fb_wpb = 0;
+  uint32_t Rc_safe = 0, fb_warp_smem = 0;
+  bool fallback = false;
+  uint32_t* d_retry = nullptr;
+  size_t retry_cap = 0;
+  double n_star_total = 0;  // fluid equilibrium prompts in service (0 = unknown)
   bool prepared = false;
 };
 
@@ -66,6 +72,31 @@ namespace {
 // Resident capacity: FCFS holds at most B prompts; WAIT at most n_j per stage
 // (invariant P14) plus one staged batch; NESTED: non-entry stages hold at
 // most n_k, entry-stage queues are bounded by memory -- take a margin.
+uint32_t round32(uint64_t x) { return (uint32_t)((std::max<uint64_t>(x, 32) + 31) & ~31ull); }
+
+// speculative (typical-case) capacity; replications that exceed it are re-run
+// with the safe capacity (derive_rc) by the fallback launch
+uint32_t speculative_rc(const sched_s* h, uint32_t safe) {
+  if (h->spec_resident_cfg) return std::min(safe, round32(h->spec_resident_cfg));
+  if (h->max_resident_cfg) return safe;
+  const auto& in = h->in;
+  uint64_t rc = safe;
+  if (in.policy == SCHED_FCFS) {
+    // FCFS residents ~ fluid prompts in service n* + margin
+    if (h->n_star_total > 0) rc = (uint64_t)(1.25 * h->n_star_total) + 64;
+  } else if (in.policy == SCHED_NESTED) {
+    // non-entry stages hold <= n_k each; entry queues stay near n_k (Lemma,
+    // PAPER.md:2345-2373) -- margin 2 n_k per boundary
+    uint64_t prev = 0, base = 0;
+    for (size_t k = 0; k < in.seg_end.size(); ++k) {
+      base += (uint64_t)in.thresholds[k] * (in.seg_end[k] - prev + (k ? 2 : 1));
+      prev = in.seg_end[k];
+    }
+    rc = base + 64;
+  }
+  return std::min(safe, round32(rc));
+}
+
 uint32_t derive_rc(const sched_s* h) {
   if (h->max_resident_cfg) return h->max_resident_cfg;
   uint64_t rc = 0;
@@ -115,30 +146,56 @@ int prepare(sched_s* h) {
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, h->device));
   h->sm_count = prop.multiProcessorCount;
-  h->Rc = derive_rc(h);
-  const int K = (int)h->in.lambda.size();
-  h->warp_smem = warp_smem_bytes(h->Rc, K);
-  // choose warps per block maximising resident warps per SM
-  int best_w = 0, best_wpb = 1, best_bps = 0;
-  const int cands[] = {8, 4, 2, 1};
-  for (int wpb : cands) {
-    const size_t smem = (size_t)wpb * h->warp_smem;
-    if (smem > (size_t)prop.sharedMemPerBlockOptin) continue;
-    // max blocks per SM from shared memory and registers (occupancy API)
-    int bps = 0;
-    const cudaError_t e = sim_occupancy(h->in.policy, 0, wpb * 32, smem, &bps);
-    if (e != cudaSuccess) return cuda_fail(e, "occupancy");
-    if (bps * wpb > best_w) { best_w = bps * wpb; best_wpb = wpb; best_bps = bps; }
+  if (h->in.policy == SCHED_FCFS && h->n_star_total == 0) {
+    sched_threshold_report rep;
+    std::vector<uint32_t> ch;
+    std::string err;
+    try {
+      if (compute_thresholds(h->in, 0, 0, 0, &rep, &ch, &err) == 0)
+        for (size_t c = 0; c < h->in.lambda.size() && c < 32; ++c) h->n_star_total += rep.n_star[c];
+    } catch (...) {
+    }
   }
-  if (best_w == 0)
-    return fail(SCHED_E_INVALID, "resident capacity too large for shared memory (max_resident=" +
-                                     std::to_string(h->Rc) + ")");
+  const int K = (int)h->in.lambda.size();
+  h->Rc_safe = derive_rc(h);
+  h->Rc = speculative_rc(h, h->Rc_safe);
+  h->fallback = h->Rc < h->Rc_safe;
+  // choose warps per block maximising resident warps per SM
+  auto size_launch = [&](uint32_t Rc, uint32_t* wsm, int* wpb_out, int* bps_out) -> int {
+    *wsm = warp_smem_bytes(Rc, K);
+    int best_w = 0;
+    const int cands[] = {8, 4, 2, 1};
+    for (int wpb : cands) {
+      const size_t smem = (size_t)wpb * *wsm;
+      if (smem > (size_t)prop.sharedMemPerBlockOptin) continue;
+      // max blocks per SM from shared memory and registers (occupancy API)
+      int bps = 0;
+      const cudaError_t e = sim_occupancy(h->in.policy, 0, wpb * 32, smem, &bps);
+      if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+      if (bps * wpb > best_w) { best_w = bps * wpb; *wpb_out = wpb; *bps_out = bps; }
+    }
+    if (best_w == 0)
+      return fail(SCHED_E_INVALID, "resident capacity too large for shared memory (max_resident=" +
+                                       std::to_string(Rc) + ")");
+    return 0;
+  };
+  int best_wpb = 1, best_bps = 0;
+  if (int rc = size_launch(h->Rc, &h->warp_smem, &best_wpb, &best_bps)) return rc;
   h->wpb = best_wpb;
   h->blocks_per_sm = best_bps;
   h->block = best_wpb * 32;
   h->grid = h->sm_count * best_bps;
+  h->fb_wpb = h->wpb; h->fb_block = h->block; h->fb_grid = 0; h->fb_warp_smem = h->warp_smem;
+  if (h->fallback) {
+    int fw = 1, fb = 0;
+    if (int rc = size_launch(h->Rc_safe, &h->fb_warp_smem, &fw, &fb)) return rc;
+    h->fb_wpb = fw;
+    h->fb_block = fw * 32;
+    h->fb_grid = h->sm_count * fb;
+  }
   const int n_rings = h->in.policy == SCHED_WAIT ? K : 1;
-  const size_t need = (size_t)h->grid * h->wpb * n_rings * h->ring_cap;
+  const size_t slots = (size_t)std::max(h->grid * h->wpb, h->fb_grid * h->fb_wpb);
+  const size_t need = slots * n_rings * h->ring_cap;
   if (need > h->ring_entries) {
     cudaFree(h->d_ring_a); cudaFree(h->d_ring_e); cudaFree(h->d_ring_llp);
     h->d_ring_a = h->d_ring_e = nullptr; h->d_ring_llp = nullptr;
@@ -147,7 +204,7 @@ int prepare(sched_s* h) {
     CK(cudaMalloc(&h->d_ring_llp, need * 4));
     h->ring_entries = need;
   }
-  if (!h->d_counter) CK(cudaMalloc(&h->d_counter, 4));
+  if (!h->d_counter) CK(cudaMalloc(&h->d_counter, 16));  // [main, fallback, retry count]
   DevParams& p = h->base;
   p.n_rings = n_rings;
   p.Rc = h->Rc;
@@ -163,12 +220,35 @@ int prepare(sched_s* h) {
 }
 
 int launch(sched_s* h, DevParams p, cudaStream_t st) {
-  CK(cudaMemsetAsync(h->d_counter, 0, 4, st));
+  CK(cudaMemsetAsync(h->d_counter, 0, 16, st));
+  p.work_counter = h->d_counter;
+  p.retry_count = h->d_counter + 2;
+  p.retry_list = nullptr;
+  p.fallback = 0;
+  if (h->fallback) {
+    if (p.n_reps > h->retry_cap) {
+      cudaFree(h->d_retry);
+      h->d_retry = nullptr;
+      CK(cudaMalloc(&h->d_retry, (size_t)p.n_reps * 4));
+      h->retry_cap = p.n_reps;
+    }
+    p.retry_list = h->d_retry;
+  }
   const size_t smem = (size_t)h->wpb * h->warp_smem;
   int grid = h->grid;
   const int warps = grid * h->wpb;
   if ((int64_t)p.n_reps < warps) grid = std::max<int>(1, (int)((p.n_reps + h->wpb - 1) / h->wpb));
   CK(launch_sim(p, grid, h->block, smem, st));
+  if (h->fallback) {
+    // replications that overflowed the speculative capacity, re-run safely
+    DevParams q = p;
+    q.fallback = 1;
+    q.work_counter = h->d_counter + 1;
+    q.Rc = h->Rc_safe;
+    q.warp_smem = h->fb_warp_smem;
+    const int fgrid = std::min(h->fb_grid, std::max(1, (int)((p.n_reps + h->fb_wpb - 1) / h->fb_wpb)));
+    CK(launch_sim(q, fgrid, h->fb_block, (size_t)h->fb_wpb * h->fb_warp_smem, st));
+  }
   return 0;
 }
 
@@ -274,6 +354,7 @@ int sched_create(sched_t* out, const sched_config* cfg) {
   }
   h->tok_budget = cfg->tok_budget;
   h->max_resident_cfg = cfg->max_resident;
+  h->spec_resident_cfg = cfg->spec_resident;
   if (cfg->restart_cap) h->ring_cap = cfg->restart_cap;
   h->device = cfg->device;
   // ticks
@@ -452,8 +533,11 @@ int sched_get_launch_info(sched_t h, sched_launch_info* out) {
   out->shared_bytes = (int32_t)(h->wpb * h->warp_smem);
   out->blocks_per_sm = h->blocks_per_sm;
   out->sm_count = h->sm_count;
-  out->max_resident = (int32_t)h->Rc;
+  out->max_resident = (int32_t)h->Rc_safe;
   out->restart_cap = (int32_t)h->ring_cap;
+  out->spec_resident = (int32_t)h->Rc;
+  out->fallback_grid = h->fallback ? h->fb_grid : 0;
+  out->fallback_warps_per_block = h->fallback ? h->fb_wpb : 0;
   return SCHED_OK;
 }
 
@@ -467,6 +551,7 @@ void sched_destroy(sched_t h) {
   cudaFree(h->d_ring_llp);
   cudaFree(h->d_counter);
   cudaFree(h->d_out);
+  cudaFree(h->d_retry);
   delete h;
 }
 

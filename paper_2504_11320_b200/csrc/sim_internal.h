@@ -44,7 +44,13 @@ struct DevParams {
   int64_t* ring_a;
   int64_t* ring_e;
   uint32_t* ring_llp;
-  uint32_t* work_counter;
+  uint32_t* work_counter;  // this launch's replication counter
+  // speculative capacity: the main launch runs with a small resident
+  // capacity; replications that overflow it are appended to retry_list and
+  // re-run from scratch by a fallback launch with the safe capacity
+  uint32_t* retry_list;    // [n_reps] (may be null: no fallback)
+  uint32_t* retry_count;
+  uint32_t fallback;       // 1: this launch processes retry_list
   // outputs
   uint64_t* out;           // field-major [SCHED_NF][n_reps]
   int64_t* log;            // trace mode: 7 int64 per batch of replication 0

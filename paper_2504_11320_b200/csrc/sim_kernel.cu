@@ -814,11 +814,19 @@ __global__ void __launch_bounds__(256) sim_kernel(const DevParams P) {
   const size_t ring_base = (size_t)slot * P.n_rings * P.ring_cap;
   WarpSim<POL, TRACE> sim(P, smem + (size_t)wib * P.warp_smem, lane, ring_base);
   for (;;) {
-    uint32_t r = 0;
-    if (lane == 0) r = atomicAdd(P.work_counter, 1u);
-    r = __shfl_sync(FULL, r, 0);
-    if (r >= P.n_reps) break;
+    uint32_t i = 0;
+    if (lane == 0) i = atomicAdd(P.work_counter, 1u);
+    i = __shfl_sync(FULL, i, 0);
+    uint32_t r = i;
+    if (P.fallback) {
+      if (i >= *P.retry_count) break;
+      r = P.retry_list[i];
+    } else if (i >= P.n_reps) {
+      break;
+    }
     sim.run(r);
+    if (!P.fallback && P.retry_list && sim.status == 1 && lane == 0)
+      P.retry_list[atomicAdd(P.retry_count, 1u)] = r;  // re-run with the safe capacity
   }
 }
 

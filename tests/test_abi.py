@@ -120,3 +120,19 @@ def test_random_threshold_agreement():
         if not fl.fluid(wl).stable:
             continue
         assert Scheduler(wl, W.Policy(W.WAIT)).thresholds()["thresholds"] == ref
+
+
+def test_ctypes_struct_sizes_match_header():
+    """The ctypes mirrors must have the C layout (a short mirror corrupts memory)."""
+    import ctypes as C
+    import subprocess
+    import tempfile
+    from paper_2504_11320_b200._lib import LaunchInfo, SchedConfig, ThresholdReport
+    src = ('#include <stdio.h>\n#include "sched.h"\nint main(){printf("%zu %zu %zu\\n",'
+           'sizeof(sched_config), sizeof(sched_threshold_report), sizeof(sched_launch_info));}')
+    with tempfile.TemporaryDirectory() as d:
+        open(os.path.join(d, "m.c"), "w").write(src)
+        subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o",
+                               os.path.join(d, "m"), os.path.join(d, "m.c")])
+        sizes = [int(x) for x in subprocess.check_output([os.path.join(d, "m")]).split()]
+    assert sizes == [C.sizeof(SchedConfig), C.sizeof(ThresholdReport), C.sizeof(LaunchInfo)]

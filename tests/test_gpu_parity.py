@@ -194,6 +194,24 @@ def test_sharding_invariance_and_determinism():
         assert np.array_equal(np.concatenate(parts, axis=1), full)
 
 
+@pytest.mark.parametrize("spec", [32, 64, 256])
+def test_speculative_capacity_fallback(spec):
+    """Replications overflowing the speculative capacity are re-run by the
+    fallback launch with the safe capacity: rows stay bit-exact."""
+    from paper_2504_11320_b200 import Scheduler
+    s = Scheduler(W.C3A, W.Policy(W.NESTED, seg_end=SEG3A), [7, 7, 7, 5], spec_resident=spec)
+    li = s.launch_info()
+    assert li["spec_resident"] == spec and li["fallback_grid"] > 0
+    got = s.run_host(W.C3A.seed, 0, 24, 20.0)
+    ref = oracle.run(W.C3A, W.Policy(W.NESTED, seg_end=SEG3A), [7, 7, 7, 5], n_reps=24, n_threads=8,
+                     horizon_s=20.0)
+    assert_rows_equal(got, ref, f"spec={spec}")
+    s2 = Scheduler(W.C2, W.Policy(W.FCFS, B=1024), spec_resident=spec)
+    got = s2.run_host(W.C2.seed, 0, 16, 2.0)
+    ref = oracle.run(W.C2, W.Policy(W.FCFS, B=1024), [0], n_reps=16, n_threads=8, horizon_s=2.0)
+    assert_rows_equal(got, ref, f"fcfs spec={spec}")
+
+
 def test_capacity_overflow_is_reported():
     rows = gpu_rows(W.C2, W.Policy(W.FCFS, B=1024), [0], 4, horizon_s=1.0, max_resident=64)
     assert (rows[oracle.F["status"]] == 1).all()

@@ -1,4 +1,5 @@
 timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-tail -30 gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; echo bench=$?
-tail -3 gpurun_out/bench.log | cut -c1-3000
+tail -15 gpurun_out/pytest_gpu.log
+rm -f gpurun_out/ab.log
+for wl in C2 C3a C4_2 C3b; do WL=$wl timeout 300 python tools/time_run.py; done > gpurun_out/ab.log 2>&1
+cat gpurun_out/ab.log
