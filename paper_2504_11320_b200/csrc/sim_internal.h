@@ -65,6 +65,7 @@ inline uint32_t warp_smem_bytes(uint32_t Rc, int K) {
   b += (uint32_t)K * (32u * 12u);           // admission windows (t, l, l')
   b += 32u * 8u;                            // staged restart ticks
   b += (64u + 32u + 32u) * 4u + 16u;        // counters, rank cursors, snapshot, align
+  b += 256u;                                // WarpStats (metric accumulators)
   return (b + 15u) & ~15u;
 }
 

@@ -147,6 +147,16 @@ __device__ __forceinline__ uint32_t count_before(const int64_t* v, uint32_t n, i
   return lo;
 }
 
+// per-replication metric accumulators, one per warp in shared memory
+// (updated once per batch by lane 0; keeps them out of the register file)
+struct __align__(16) WarpStats {
+  u128 sum_done_t, sum_ft_t;            // sum over batches of n * t_end
+  u128 acc_arr, acc_done_a, acc_ft_a;   // flushed lane-local arrival-tick sums
+  uint64_t arrivals, admitted, completed, completed_after_T, completed_tokens, first_tokens,
+      batches, request_steps, prefill_steps, evictions, cbi, sum_waiting, h;
+  int64_t busy, idle, max_kv, log_n;
+};
+
 template <int POL, bool TRACE>
 struct WarpSim {
   const DevParams& P;
@@ -161,6 +171,7 @@ struct WarpSim {
   uint32_t* cnt;                     // [64] WAIT: residents per class; NESTED: [k] / [32+k]
   uint32_t* rank;                    // [32] NESTED per-segment rank cursors
   uint32_t* snap;                    // [32] NESTED entry counts at decision time
+  WarpStats* st;                     // metric accumulators
   size_t ring_base;                  // first ring entry of this warp slot
 
   // per-class cursor state, lane c holds class c (and ring c for WAIT; ring 0
@@ -177,12 +188,8 @@ struct WarpSim {
   int64_t now, KV;
   uint32_t n_res, n_new, status;
   int64_t sum_new_l;
-  uint64_t arrivals, admitted, completed, completed_after_T, completed_tokens, first_tokens,
-      batches, request_steps, prefill_steps, evictions, cbi, sum_waiting;
-  int64_t busy, idle, max_kv;
-  uint64_t h;
-  u128 acc_lat, acc_ttft, acc_arr, acc_arr_done;  // lane-local partial sums
-  int64_t log_n;
+  // lane-local partial sums of arrival ticks (flushed to st before they can overflow)
+  uint64_t acc_arr, acc_done_a, acc_ft_a;
   // per-epoch plan
   uint32_t Qmask;     // WAIT: qualifying classes
   int kstar;          // NESTED: last active segment
@@ -201,6 +208,16 @@ struct WarpSim {
     cnt = (uint32_t*)(((uintptr_t)(alp + p.K * 32) + 15) & ~(uintptr_t)15);
     rank = cnt + 64;
     snap = rank + 32;
+    st = (WarpStats*)(snap + 32);
+  }
+
+  __device__ void flush_acc() {
+    const u128 a = warp_sum_u128(acc_arr), b = warp_sum_u128(acc_done_a), c = warp_sum_u128(acc_ft_a);
+    if (lane == 0) { st->acc_arr += a; st->acc_done_a += b; st->acc_ft_a += c; }
+    acc_arr = acc_done_a = acc_ft_a = 0;
+  }
+  __device__ __forceinline__ void maybe_flush() {
+    if (__any_sync(FULL, ((acc_arr | acc_done_a | acc_ft_a) >> 60) != 0)) flush_acc();
   }
 
   __device__ __forceinline__ size_t ring_slot(int q, uint32_t pos) const {
@@ -274,12 +291,14 @@ struct WarpSim {
         const int64_t t = vt[c * 32 + lane];
         const bool vis = (uint32_t)lane >= j && t <= now && t < P.T_t;
         const uint32_t n = __popc(__ballot_sync(FULL, vis));
-        if (vis) acc_arr += (u128)(uint64_t)t;
-        arrivals += n;
+        if (vis) acc_arr += (uint64_t)t;
+        if (lane == 0) st->arrivals += n;
         if (lane == c) k_vis += n;
         if (j + n < 32) break;
+        maybe_flush();
       }
     }
+    maybe_flush();
   }
 
   // next not-yet-visible arrival tick (< T), TMAX if none
@@ -569,7 +588,7 @@ struct WarpSim {
       KV -= (int64_t)__reduce_add_sync(FULL, ev ? (l + s - 1) : 0u);
       n_plan_res -= __reduce_add_sync(FULL, ev ? inp : 0u);
       n_res -= ne;
-      evictions += ne;
+      if (lane == 0) st->evictions += ne;
       n_evict += ne;
       __syncwarp();
     }
@@ -682,34 +701,41 @@ struct WarpSim {
     // tau = d0 + d1 * (sum prefill l + sum decode (l+s))
     const int64_t tau = P.d0_t + P.d1_t * tokens;
     const int64_t t_end = now + tau;
-    if (t_end <= P.T_t) {
-      acc_lat += (u128)((uint64_t)n_done * (uint64_t)t_end - done_a);
-      acc_ttft += (u128)((uint64_t)n_ft * (uint64_t)t_end - ft_a);
-      acc_arr_done += (u128)done_a;
-      completed += nd;
-      completed_tokens += dtok;
-      first_tokens += nf;
-      cbi += (uint64_t)nd * batches;
-    } else {
-      completed_after_T += nd;
-    }
+    const bool by_T = t_end <= P.T_t;
+    if (by_T) { acc_done_a += done_a; acc_ft_a += ft_a; }
     KV += (int64_t)gr - (int64_t)kvf + sum_new_l;
     const uint32_t plan_size = n_plan_res + n_new;
-    if (TRACE && rep == 0 && lane == 0 && log_n < P.log_cap) {
-      int64_t* e = P.log + 7 * log_n;
-      e[0] = now; e[1] = plan_size; e[2] = tokens; e[3] = nd; e[4] = n_evict; e[5] = n_new; e[6] = peak;
+    if (lane == 0) {
+      if (by_T) {
+        // latency / TTFT sums = sum(t_end) - sum(a)
+        st->sum_done_t += (u128)nd * (uint64_t)t_end;
+        st->sum_ft_t += (u128)nf * (uint64_t)t_end;
+        st->completed += nd;
+        st->completed_tokens += dtok;
+        st->first_tokens += nf;
+        st->cbi += (uint64_t)nd * st->batches;
+      } else {
+        st->completed_after_T += nd;
+      }
+      if (TRACE && rep == 0 && st->log_n < P.log_cap) {
+        int64_t* e = P.log + 7 * st->log_n;
+        e[0] = now; e[1] = plan_size; e[2] = tokens; e[3] = nd; e[4] = n_evict; e[5] = n_new; e[6] = peak;
+      }
+      if (TRACE && rep == 0) ++st->log_n;
+      uint64_t hh = st->h;
+      hh = mix64(hh ^ (uint64_t)now);
+      hh = mix64(hh ^ ((uint64_t)plan_size | ((uint64_t)tokens << 32)));
+      hh = mix64(hh ^ ((uint64_t)nd | ((uint64_t)n_evict << 20) | ((uint64_t)n_new << 40)));
+      st->h = hh;
+      st->request_steps += plan_size;
+      st->prefill_steps += n_new;
+      st->admitted += n_new;
+      st->busy += tau;
+      if (peak > st->max_kv) st->max_kv = peak;
+      st->sum_waiting += waiting;
+      ++st->batches;
     }
-    if (TRACE && rep == 0) ++log_n;
-    h = mix64(h ^ (uint64_t)now);
-    h = mix64(h ^ ((uint64_t)plan_size | ((uint64_t)tokens << 32)));
-    h = mix64(h ^ ((uint64_t)nd | ((uint64_t)n_evict << 20) | ((uint64_t)n_new << 40)));
-    request_steps += plan_size;
-    prefill_steps += n_new;
-    admitted += n_new;
-    busy += tau;
-    if (peak > max_kv) max_kv = peak;
-    sum_waiting += waiting;
-    ++batches;
+    maybe_flush();
     n_res = wp;
     n_new = 0;
     now = t_end;
@@ -721,13 +747,15 @@ struct WarpSim {
     rep = rep_;
     rglob = (uint32_t)(P.rep_begin + rep_);
     const uint64_t seed = TRACE ? 0ull : P.seed;
-    h = mix64(seed ^ ((uint64_t)(TRACE ? rep_ : rglob) * 0x9E3779B97F4A7C15ull));
     now = 0; KV = 0; n_res = 0; n_new = 0; status = 0; sum_new_l = 0;
-    arrivals = admitted = completed = completed_after_T = completed_tokens = first_tokens = 0;
-    batches = request_steps = prefill_steps = evictions = cbi = sum_waiting = 0;
-    busy = idle = max_kv = 0;
-    acc_lat = acc_ttft = acc_arr = acc_arr_done = 0;
-    log_n = 0;
+    acc_arr = acc_done_a = acc_ft_a = 0;
+    __syncwarp();
+    if (lane == 0) {
+      WarpStats z = {};
+      z.h = mix64(seed ^ ((uint64_t)(TRACE ? rep_ : rglob) * 0x9E3779B97F4A7C15ull));
+      *st = z;
+    }
+    __syncwarp();
     k_vis = vbase = k_adm = abase = rhead = rtail = 0;
     vprev = aprev = 0;
     newc = 0;
@@ -754,7 +782,7 @@ struct WarpSim {
       if (!go) {
         const int64_t nt = next_arrival();
         if (nt == TMAX) break;
-        idle += nt - now;
+        if (lane == 0) st->idle += nt - now;
         now = nt;
         continue;
       }
@@ -765,48 +793,51 @@ struct WarpSim {
 
   __device__ void finish() {
     const uint32_t waiting = waiting_total();
-    const u128 lat = warp_sum_u128(acc_lat);
-    const u128 ttft = warp_sum_u128(acc_ttft);
-    const u128 arr = warp_sum_u128(acc_arr);
-    const u128 arr_done = warp_sum_u128(acc_arr_done);
-    const u128 soj = lat + (u128)(arrivals - completed) * (u128)(uint64_t)P.T_t - (arr - arr_done);
+    flush_acc();
+    __syncwarp();
+    const WarpStats S = *st;
+    const uint64_t arrivals = S.arrivals, completed = S.completed;
+    const u128 lat = S.sum_done_t - S.acc_done_a;
+    const u128 ttft = S.sum_ft_t - S.acc_ft_a;
+    // sum over arrivals of min(c, T) - a
+    const u128 soj = lat + (u128)(arrivals - completed) * (u128)(uint64_t)P.T_t - (S.acc_arr - S.acc_done_a);
     uint64_t v = 0;
     switch (lane) {
       case SCHED_F_ARRIVALS: v = arrivals; break;
-      case SCHED_F_ADMITTED: v = admitted; break;
+      case SCHED_F_ADMITTED: v = S.admitted; break;
       case SCHED_F_COMPLETED: v = completed; break;
-      case SCHED_F_COMPLETED_AFTER_T: v = completed_after_T; break;
-      case SCHED_F_COMPLETED_TOKENS: v = completed_tokens; break;
-      case SCHED_F_FIRST_TOKENS: v = first_tokens; break;
-      case SCHED_F_BATCHES: v = batches; break;
-      case SCHED_F_REQUEST_STEPS: v = request_steps; break;
-      case SCHED_F_PREFILL_STEPS: v = prefill_steps; break;
-      case SCHED_F_EVICTIONS: v = evictions; break;
-      case SCHED_F_BUSY_TICKS: v = (uint64_t)busy; break;
-      case SCHED_F_IDLE_TICKS: v = (uint64_t)idle; break;
+      case SCHED_F_COMPLETED_AFTER_T: v = S.completed_after_T; break;
+      case SCHED_F_COMPLETED_TOKENS: v = S.completed_tokens; break;
+      case SCHED_F_FIRST_TOKENS: v = S.first_tokens; break;
+      case SCHED_F_BATCHES: v = S.batches; break;
+      case SCHED_F_REQUEST_STEPS: v = S.request_steps; break;
+      case SCHED_F_PREFILL_STEPS: v = S.prefill_steps; break;
+      case SCHED_F_EVICTIONS: v = S.evictions; break;
+      case SCHED_F_BUSY_TICKS: v = (uint64_t)S.busy; break;
+      case SCHED_F_IDLE_TICKS: v = (uint64_t)S.idle; break;
       case SCHED_F_LAT_LO: v = (uint64_t)lat; break;
       case SCHED_F_LAT_HI: v = (uint64_t)(lat >> 64); break;
       case SCHED_F_TTFT_LO: v = (uint64_t)ttft; break;
       case SCHED_F_TTFT_HI: v = (uint64_t)(ttft >> 64); break;
       case SCHED_F_SOJ_LO: v = (uint64_t)soj; break;
       case SCHED_F_SOJ_HI: v = (uint64_t)(soj >> 64); break;
-      case SCHED_F_COMPLETION_BATCH_IDX: v = cbi; break;
-      case SCHED_F_MAX_KV_PEAK: v = (uint64_t)max_kv; break;
+      case SCHED_F_COMPLETION_BATCH_IDX: v = S.cbi; break;
+      case SCHED_F_MAX_KV_PEAK: v = (uint64_t)S.max_kv; break;
       case SCHED_F_FINAL_WAITING: v = waiting; break;
       case SCHED_F_FINAL_RESIDENT: v = n_res; break;
-      case SCHED_F_TRAJ_HASH: v = h; break;
+      case SCHED_F_TRAJ_HASH: v = S.h; break;
       case SCHED_F_STATUS: v = status; break;
       case SCHED_F_NOW_STOP: v = (uint64_t)now; break;
-      case SCHED_F_SUM_WAITING: v = sum_waiting; break;
+      case SCHED_F_SUM_WAITING: v = S.sum_waiting; break;
       default: break;
     }
     if (lane < SCHED_NF) P.out[(size_t)lane * P.n_reps + rep] = v;
-    if (TRACE && rep == 0 && lane == 0) *P.log_n = log_n;
+    if (TRACE && rep == 0 && lane == 0) *P.log_n = S.log_n;
   }
 };
 
 template <int POL, bool TRACE>
-__global__ void __launch_bounds__(256) sim_kernel(const DevParams P) {
+__global__ void __launch_bounds__(256, POL == SCHED_WAIT ? 3 : 2) sim_kernel(const DevParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
