@@ -28,7 +28,10 @@ typedef struct sched_s* sched_t;
 enum {
   SCHED_WAIT = 0,    /* Algorithm 1: per-type thresholds n_j */
   SCHED_NESTED = 1,  /* Algorithm 2: per-segment thresholds n_k */
-  SCHED_FCFS = 2     /* vLLM-style new-first FCFS baseline */
+  SCHED_FCFS = 2,    /* vLLM-style new-first FCFS baseline */
+  SCHED_FCFS_ONGOING = 3  /* Sarathi-style ongoing-first FCFS (R29):
+                             new prompts are admitted only if they fit after the
+                             ongoing prompts' growth */
 };
 
 /* error codes */
@@ -89,14 +92,14 @@ typedef struct {
   double d0_s;                /* tau = d0 + d1 * tokens (Eq. time_consump) */
   double d1_s;
   int64_t M;                  /* KV capacity C in tokens (Eq. memory_constraint) */
-  int32_t policy;             /* SCHED_WAIT / SCHED_NESTED / SCHED_FCFS */
+  int32_t policy;             /* SCHED_WAIT / SCHED_NESTED / SCHED_FCFS / SCHED_FCFS_ONGOING */
   uint32_t n_thr;             /* WAIT: K; NESTED: n_seg; 0 = set later by sched_thresholds */
   const uint32_t* thresholds; /* host [n_thr], each >= 1 */
   uint32_t n_seg;             /* NESTED: number of segments L (1..32) */
   const uint16_t* seg_end;    /* host [n_seg]: last stage of each segment, increasing,
                                  seg_end[0] >= 1, seg_end[L-1] >= max l' */
-  uint32_t B;                 /* FCFS: max resident prompts (>= 1); WAIT heuristic B */
-  uint32_t tok_budget;        /* FCFS: max prefill tokens per iteration (0 = none) */
+  uint32_t B;                 /* FCFS*: max resident prompts (>= 1); WAIT heuristic B */
+  uint32_t tok_budget;        /* FCFS*: max prefill tokens per iteration (0 = none) */
   uint32_t max_resident;      /* per-replication resident capacity (0 = derive) */
   uint32_t restart_cap;       /* per-FIFO restart ring capacity (0 = default 8192) */
   uint32_t spec_resident;     /* speculative capacity of the main launch (0 = derive);

@@ -32,7 +32,7 @@ FIELDS = [
 NF = len(FIELDS)
 F = {n: i for i, n in enumerate(FIELDS)}
 
-WAIT, NESTED, FCFS = 0, 1, 2
+WAIT, NESTED, FCFS, FCFS_ONGOING = 0, 1, 2, 3
 
 
 def build(force: bool = False) -> str:

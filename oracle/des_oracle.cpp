@@ -319,13 +319,17 @@ struct Sim {
     // reading R15): every resident decodes, then admit the FIFO head in
     // order while the batch-size limit, the current-KV check and the prefill
     // token budget all hold; stop at the first candidate that fails.
+    // Sarathi-style "ongoing first" (reading R29) differs in
+    // one term: the KV check also reserves the residents' growth of one
+    // token each, so only what fits after the ongoing prompts is admitted.
     for (size_t i = 0; i < res.size(); ++i) P.res_in[i] = 1;
+    const int64_t reserve = S.policy == ORC_FCFS_ONGOING ? (int64_t)res.size() : 0;
     int64_t new_l = 0;
     uint64_t n_new = 0;
     for (size_t j = 0; j < fifo[0].size(); ++j) {
       const Prompt& p = fifo[0][j];
       if ((uint64_t)res.size() + n_new >= S.B) break;
-      if (KV + new_l + p.l > S.M) break;
+      if (KV + reserve + new_l + p.l > S.M) break;
       if (S.tok_budget != 0 && (uint64_t)(new_l + p.l) > S.tok_budget) break;
       new_l += p.l; ++n_new;
       P.new_fifo.push_back(0); P.new_pos.push_back((int)j);

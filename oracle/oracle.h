@@ -13,7 +13,7 @@
 extern "C" {
 #endif
 
-enum { ORC_WAIT = 0, ORC_NESTED = 1, ORC_FCFS = 2 };
+enum { ORC_WAIT = 0, ORC_NESTED = 1, ORC_FCFS = 2, ORC_FCFS_ONGOING = 3 };
 
 /* metric row fields (field-major output: out[f * n_reps + i]) */
 enum {
@@ -37,7 +37,7 @@ typedef struct {
   const uint64_t* lp_w;
   double d0_s, d1_s;         /* batch time tau = d0 + d1 * tokens (seconds) */
   int64_t M;                 /* KV capacity, tokens */
-  int32_t policy;            /* ORC_WAIT / ORC_NESTED / ORC_FCFS */
+  int32_t policy;            /* ORC_WAIT / ORC_NESTED / ORC_FCFS / ORC_FCFS_ONGOING */
   int32_t n_thr;             /* WAIT: K thresholds; NESTED: n_seg thresholds */
   const uint32_t* thr;
   int32_t n_seg;             /* NESTED: number of segments */

@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsched.so")
 
-WAIT, NESTED, FCFS = 0, 1, 2
+WAIT, NESTED, FCFS, FCFS_ONGOING = 0, 1, 2, 3
 ERRORS = {-1: "SCHED_E_INVALID", -2: "SCHED_E_UNSTABLE", -3: "SCHED_E_INFEASIBLE",
           -4: "SCHED_E_UNSATISFIABLE", -5: "SCHED_E_CUDA", -6: "SCHED_E_CAPACITY"}
 
@@ -150,7 +150,7 @@ class Scheduler:
         cfg.d0_s, cfg.d1_s, cfg.M = workload.d0_s, workload.d1_s, workload.M
         cfg.policy = policy.kind
         thr = list(thresholds) if thresholds is not None else list(policy.thresholds or [])
-        if policy.kind == FCFS:
+        if policy.kind in (FCFS, FCFS_ONGOING):
             thr = []
         a, p = _arr(thr or [0], np.uint32)
         keep.append(a)

@@ -69,6 +69,8 @@ struct sched_s {
 
 namespace {
 
+bool is_fcfs(int policy) { return policy == SCHED_FCFS || policy == SCHED_FCFS_ONGOING; }
+
 // Resident capacity: FCFS holds at most B prompts; WAIT at most n_j per stage
 // (invariant P14) plus one staged batch; NESTED: non-entry stages hold at
 // most n_k, entry-stage queues are bounded by memory -- take a margin.
@@ -81,7 +83,7 @@ uint32_t speculative_rc(const sched_s* h, uint32_t safe) {
   if (h->max_resident_cfg) return safe;
   const auto& in = h->in;
   uint64_t rc = safe;
-  if (in.policy == SCHED_FCFS) {
+  if (is_fcfs(in.policy)) {
     // FCFS residents ~ fluid prompts in service n* + margin
     if (h->n_star_total > 0) rc = (uint64_t)(1.25 * h->n_star_total) + 64;
   } else if (in.policy == SCHED_NESTED) {
@@ -101,7 +103,7 @@ uint32_t derive_rc(const sched_s* h) {
   if (h->max_resident_cfg) return h->max_resident_cfg;
   uint64_t rc = 0;
   const auto& in = h->in;
-  if (in.policy == SCHED_FCFS) {
+  if (is_fcfs(in.policy)) {
     rc = in.B;
   } else if (in.policy == SCHED_WAIT) {
     for (size_t c = 0; c < in.thresholds.size(); ++c) {
@@ -127,7 +129,7 @@ uint32_t derive_rc(const sched_s* h) {
 
 int prepare(sched_s* h) {
   if (h->prepared) return 0;
-  if (h->in.policy != SCHED_FCFS && h->in.thresholds.empty())
+  if (!is_fcfs(h->in.policy) && h->in.thresholds.empty())
     return fail(SCHED_E_INVALID, "thresholds not set: pass them in sched_config or call sched_thresholds");
   CK(cudaSetDevice(h->device));
   if (!h->d_cdf_thr) {
@@ -146,7 +148,7 @@ int prepare(sched_s* h) {
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, h->device));
   h->sm_count = prop.multiProcessorCount;
-  if (h->in.policy == SCHED_FCFS && h->n_star_total == 0) {
+  if (is_fcfs(h->in.policy) && h->n_star_total == 0) {
     sched_threshold_report rep;
     std::vector<uint32_t> ch;
     std::string err;
@@ -275,7 +277,7 @@ int sched_create(sched_t* out, const sched_config* cfg) {
     return fail(SCHED_E_INVALID, "null table pointer");
   if (!(cfg->d0_s > 0) || !(cfg->d1_s >= 0)) return fail(SCHED_E_INVALID, "need d0 > 0, d1 >= 0");
   if (cfg->M < 1) return fail(SCHED_E_INVALID, "M must be >= 1");
-  if (cfg->policy < SCHED_WAIT || cfg->policy > SCHED_FCFS) return fail(SCHED_E_INVALID, "bad policy");
+  if (cfg->policy < SCHED_WAIT || cfg->policy > SCHED_FCFS_ONGOING) return fail(SCHED_E_INVALID, "bad policy");
   sched_s* h = new sched_s();
   SetupInput& in = h->in;
   in.d0_s = cfg->d0_s; in.d1_s = cfg->d1_s; in.M = cfg->M; in.policy = cfg->policy; in.B = cfg->B;
@@ -329,7 +331,7 @@ int sched_create(sched_t* out, const sched_config* cfg) {
   }
   h->max_lp = max_lp;
   h->min_l = min_l;
-  if (cfg->policy == SCHED_FCFS) {
+  if (is_fcfs(cfg->policy)) {
     if (cfg->B < 1) { delete h; return fail(SCHED_E_INVALID, "FCFS needs B >= 1"); }
     if (cfg->tok_budget && cfg->tok_budget < max_l) { delete h; return fail(SCHED_E_INVALID, "tok_budget below the largest prefill length"); }
   }
@@ -345,7 +347,7 @@ int sched_create(sched_t* out, const sched_config* cfg) {
     if (in.seg_end.back() < max_lp) { delete h; return fail(SCHED_E_INVALID, "last segment must reach max l'"); }
   }
   const uint32_t want_thr = cfg->policy == SCHED_WAIT ? K : cfg->policy == SCHED_NESTED ? cfg->n_seg : 0;
-  if (cfg->n_thr && cfg->policy != SCHED_FCFS) {
+  if (cfg->n_thr && !is_fcfs(cfg->policy)) {
     if (cfg->n_thr != want_thr || !cfg->thresholds) { delete h; return fail(SCHED_E_INVALID, "threshold count mismatch"); }
     for (uint32_t i = 0; i < cfg->n_thr; ++i) {
       if (cfg->thresholds[i] < 1) { delete h; return fail(SCHED_E_INVALID, "thresholds must be >= 1"); }
@@ -399,7 +401,7 @@ int sched_thresholds(sched_t h, int32_t mode, double delta, double budget_B,
   } catch (const std::exception& ex) {
     return fail(SCHED_E_INVALID, ex.what());
   }
-  if (rc == -2 && chosen.empty() && h->in.policy != SCHED_FCFS && h->in.thresholds.empty())
+  if (rc == -2 && chosen.empty() && !is_fcfs(h->in.policy) && h->in.thresholds.empty())
     return fail(SCHED_E_UNSTABLE, err.empty() ? "rho >= 1" : err);
   if (rc == -3) return fail(SCHED_E_INFEASIBLE, err);
   if (rc == -1) return fail(SCHED_E_INVALID, err);

@@ -70,7 +70,6 @@ inline uint32_t warp_smem_bytes(uint32_t Rc, int K) {
 }
 
 cudaError_t launch_sim(const DevParams& p, int grid, int block, size_t smem, cudaStream_t s);
-int sim_regs_per_thread(int policy, int trace);
 cudaError_t sim_occupancy(int policy, int trace, int block, size_t smem, int* blocks_per_sm);
 
 }  // namespace waitsim

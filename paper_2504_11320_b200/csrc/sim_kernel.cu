@@ -414,7 +414,9 @@ struct WarpSim {
       if (FCFS_COND) {
         const uint32_t pre = warp_incl_scan_u32(l, lane);
         const bool ok = (uint32_t)lane < m && (n_res + n_new + lane < P.B) &&
-                        (KV + sum_new_l + (int64_t)pre <= P.M) &&
+                        // Sarathi-style ongoing-first also reserves the residents' growth (R29)
+                        (KV + (POL == SCHED_FCFS_ONGOING ? (int64_t)n_res : 0) + sum_new_l +
+                             (int64_t)pre <= P.M) &&
                         (P.tok_budget == 0 || sum_new_l + (int64_t)pre <= (int64_t)P.tok_budget);
         const uint32_t okm = __ballot_sync(FULL, ok);  // ok lanes form a prefix
         take = okm == FULL ? 32u : (uint32_t)__ffs(~okm) - 1;
@@ -533,7 +535,7 @@ struct WarpSim {
       const uint32_t l = (uint32_t)(qv & 0xFFFF), lp = (uint32_t)((qv >> 16) & 0xFFFF);
       const uint32_t s = (uint32_t)((qv >> 32) & 0xFFFF), meta = (uint32_t)(qv >> 48);
       uint32_t inp = 0, nkey = 0;
-      if (POL == SCHED_FCFS) inp = valid;
+      if (POL == SCHED_FCFS || POL == SCHED_FCFS_ONGOING) inp = valid;
       if (POL == SCHED_WAIT) inp = valid && ((Qmask >> (meta & 0xFF)) & 1u);
       if (POL == SCHED_NESTED) {
         const uint32_t info = valid ? __ldg(P.stage_info + s) : 0u;
@@ -878,12 +880,6 @@ cudaError_t occ_t(int block, size_t smem, int* bps) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k, block, smem);
 }
 
-template <int POL, bool TRACE>
-int regs_t() {
-  cudaFuncAttributes a;
-  if (cudaFuncGetAttributes(&a, sim_kernel<POL, TRACE>) != cudaSuccess) return -1;
-  return a.numRegs;
-}
 
 }  // namespace
 
@@ -892,12 +888,14 @@ cudaError_t launch_sim(const DevParams& p, int grid, int block, size_t smem, cud
     switch (p.policy) {
       case SCHED_WAIT: return launch_t<SCHED_WAIT, true>(p, grid, block, smem, s);
       case SCHED_NESTED: return launch_t<SCHED_NESTED, true>(p, grid, block, smem, s);
+      case SCHED_FCFS_ONGOING: return launch_t<SCHED_FCFS_ONGOING, true>(p, grid, block, smem, s);
       default: return launch_t<SCHED_FCFS, true>(p, grid, block, smem, s);
     }
   }
   switch (p.policy) {
     case SCHED_WAIT: return launch_t<SCHED_WAIT, false>(p, grid, block, smem, s);
     case SCHED_NESTED: return launch_t<SCHED_NESTED, false>(p, grid, block, smem, s);
+    case SCHED_FCFS_ONGOING: return launch_t<SCHED_FCFS_ONGOING, false>(p, grid, block, smem, s);
     default: return launch_t<SCHED_FCFS, false>(p, grid, block, smem, s);
   }
 }
@@ -907,28 +905,15 @@ cudaError_t sim_occupancy(int policy, int trace, int block, size_t smem, int* bp
     switch (policy) {
       case SCHED_WAIT: return occ_t<SCHED_WAIT, true>(block, smem, bps);
       case SCHED_NESTED: return occ_t<SCHED_NESTED, true>(block, smem, bps);
+      case SCHED_FCFS_ONGOING: return occ_t<SCHED_FCFS_ONGOING, true>(block, smem, bps);
       default: return occ_t<SCHED_FCFS, true>(block, smem, bps);
     }
   }
   switch (policy) {
     case SCHED_WAIT: return occ_t<SCHED_WAIT, false>(block, smem, bps);
     case SCHED_NESTED: return occ_t<SCHED_NESTED, false>(block, smem, bps);
+    case SCHED_FCFS_ONGOING: return occ_t<SCHED_FCFS_ONGOING, false>(block, smem, bps);
     default: return occ_t<SCHED_FCFS, false>(block, smem, bps);
-  }
-}
-
-int sim_regs_per_thread(int policy, int trace) {
-  if (trace) {
-    switch (policy) {
-      case SCHED_WAIT: return regs_t<SCHED_WAIT, true>();
-      case SCHED_NESTED: return regs_t<SCHED_NESTED, true>();
-      default: return regs_t<SCHED_FCFS, true>();
-    }
-  }
-  switch (policy) {
-    case SCHED_WAIT: return regs_t<SCHED_WAIT, false>();
-    case SCHED_NESTED: return regs_t<SCHED_NESTED, false>();
-    default: return regs_t<SCHED_FCFS, false>();
   }
 }
 

@@ -30,7 +30,7 @@ def _cuda():
 
 def gpu_rows(wl, pol, thr, n, horizon_s=None, rep_begin=0, seed=None, **kw):
     from paper_2504_11320_b200 import Scheduler
-    s = Scheduler(wl, pol, None if pol.kind == W.FCFS else thr, **kw)
+    s = Scheduler(wl, pol, thr, **kw)
     out = s.run_host(wl.seed if seed is None else seed, rep_begin, n,
                      wl.horizon_s if horizon_s is None else horizon_s)
     s.close()
@@ -60,6 +60,7 @@ def test_c1_all_policies():
     check(W.C1, W.Policy(W.WAIT), [1], 64)          # LIFO-eviction regime (M < M^pi)
     check(W.C1P, W.Policy(W.WAIT), [1], 64)         # eviction-free
     check(W.C1, W.Policy(W.FCFS, B=32), [0], 64)
+    check(W.C1, W.Policy(W.FCFS_ONGOING, B=32), [0], 64)
     check(W.C1, W.Policy(W.NESTED, seg_end=[16]), [1], 64)
     check(W.C1, W.Policy(W.WAIT), [3], 32)
 
@@ -68,6 +69,7 @@ def test_c2_wait_fluid_heuristic_fcfs():
     check(W.C2, W.Policy(W.WAIT), fl.wait_fluid_integer(W.C2), 48, horizon_s=2.0)
     check(W.C2, W.Policy(W.WAIT), fl.wait_heuristic(W.C2, 1024), 48, horizon_s=2.0)
     check(W.C2, W.Policy(W.FCFS, B=1024), [0], 48, horizon_s=2.0)
+    check(W.C2, W.Policy(W.FCFS_ONGOING, B=1024), [0], 48, horizon_s=2.0)
 
 
 def test_c2_full_horizon_sample():
@@ -92,6 +94,7 @@ def test_c4_rate_sweep(i):
     check(wl, W.Policy(W.WAIT), fl.wait_fluid_integer(wl), 12, horizon_s=8.0)
     check(wl, W.Policy(W.NESTED, seg_end=SEG4), fl.nested_strict(wl, SEG4), 12, horizon_s=8.0)
     check(wl, W.Policy(W.FCFS, B=1024), [0], 12, horizon_s=8.0)
+    check(wl, W.Policy(W.FCFS_ONGOING, B=1024), [0], 12, horizon_s=8.0)
 
 
 @pytest.mark.parametrize("qps", [55.0, 110.0])
@@ -100,6 +103,7 @@ def test_c5_chat_shaped(qps):
     kw = dict(max_resident=4096, restart_cap=1 << 16)
     check(wl, W.Policy(W.NESTED, seg_end=SEG10), W.PAPER_NESTED_RATIO_C5, 8, horizon_s=120.0, **kw)
     check(wl, W.Policy(W.FCFS, B=1024), [0], 8, horizon_s=120.0, **kw)
+    check(wl, W.Policy(W.FCFS_ONGOING, B=1024), [0], 8, horizon_s=120.0, **kw)
 
 
 # ------------------------------------------------- random small systems
@@ -110,18 +114,20 @@ def test_random_small_workloads(seed):
     maxlp = max(v for t in wl.lp_tab for v, _ in t)
     seg = sorted({int(x) for x in rng.integers(1, maxlp + 1, 2)} | {maxlp})
     check(wl, W.Policy(W.WAIT), [int(rng.integers(1, 5)) for _ in range(wl.K)], 16)
-    check(wl, W.Policy(W.FCFS, B=int(rng.integers(1, 40)),
-                       tok_budget=int(rng.choice([0, 0, 12]))), [0], 16)
+    for fk in (W.FCFS, W.FCFS_ONGOING):
+        check(wl, W.Policy(fk, B=int(rng.integers(1, 40)),
+                           tok_budget=int(rng.choice([0, 0, 12]))), [0], 16)
     check(wl, W.Policy(W.NESTED, seg_end=seg),
           sorted([int(x) for x in rng.integers(1, 5, len(seg))], reverse=True), 16)
 
 
 # --------------------------------------------------------- explicit traces
-def test_example2_trace_log():
+@pytest.mark.parametrize("kind", [W.FCFS, W.FCFS_ONGOING])
+def test_example2_trace_log(kind):
     from paper_2504_11320_b200 import Scheduler
     from test_oracle import _ex2_trace
     tr, t_end = _ex2_trace()
-    pol = W.Policy(W.FCFS, B=1000)
+    pol = W.Policy(kind, B=1000)
     ref_rows, ref_log = oracle.run_trace(W.EX2, pol, [0], [tr], log_cap=32, horizon_s=t_end / 1e12)
     s = Scheduler(W.EX2, pol)
     rows, log = s.run_trace([tr], t_end / 1e12, log_cap=32)
@@ -143,10 +149,11 @@ def test_bruteforce_tiny_traces():
         for M in range(l + lp, 9):
             wl = W.Workload("bf", [1.0], [W.fixed(l)], [W.fixed(lp)], M=M, horizon_s=0.1,
                             seed=0, d0_s=0.005, d1_s=0.001)
-            for pol, thr in [(W.Policy(W.FCFS, B=3), [0]), (W.Policy(W.WAIT), [1]),
-                             (W.Policy(W.WAIT), [2]), (W.Policy(W.NESTED, seg_end=[lp]), [2])]:
+            for pol, thr in [(W.Policy(W.FCFS, B=3), [0]), (W.Policy(W.FCFS_ONGOING, B=3), [0]),
+                             (W.Policy(W.WAIT), [1]), (W.Policy(W.WAIT), [2]),
+                             (W.Policy(W.NESTED, seg_end=[lp]), [2])]:
                 ref, _ = oracle.run_trace(wl, pol, thr, traces)
-                s = Scheduler(wl, pol, None if pol.kind == W.FCFS else thr)
+                s = Scheduler(wl, pol, thr)
                 got, _ = s.run_trace(traces, 0.1)
                 s.close()
                 assert_rows_equal(got, ref, f"bf l={l} lp={lp} M={M} pol={pol.kind}")
@@ -172,12 +179,13 @@ def test_multiclass_traces_with_ties():
             traces.append([(t, c, l[c], lp[c]) for t, c in tr])
         maxlp = max(lp)
         for pol, thr in [(W.Policy(W.FCFS, B=int(rng.integers(1, 10))), [0]),
+                         (W.Policy(W.FCFS_ONGOING, B=int(rng.integers(1, 10))), [0]),
                          (W.Policy(W.WAIT), [int(rng.integers(1, 4)) for _ in range(K)]),
                          (W.Policy(W.NESTED, seg_end=sorted({1, maxlp})), None)]:
             if thr is None:
                 thr = sorted([int(x) for x in rng.integers(1, 4, len(pol.seg_end))], reverse=True)
             ref, _ = oracle.run_trace(wl, pol, thr, traces)
-            s = Scheduler(wl, pol, None if pol.kind == W.FCFS else thr)
+            s = Scheduler(wl, pol, thr)
             got, _ = s.run_trace(traces, 0.2)
             s.close()
             assert_rows_equal(got, ref, f"trial {trial} pol {pol.kind}")

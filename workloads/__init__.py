@@ -35,8 +35,8 @@ D0_S = 0.012        # 12 ms fixed iteration overhead (SURVEY A21 reading)
 D1_S = 0.35e-6      # 0.35 us per KV token (SURVEY A21 reading)
 M_7B = 131_072      # tokens: 64 GiB / 512 KiB per token of fp16 Llama-2-7B KV
 
-WAIT, NESTED, FCFS = 0, 1, 2
-POLICY_NAMES = {WAIT: "wait", NESTED: "nested", FCFS: "fcfs"}
+WAIT, NESTED, FCFS, FCFS_ONGOING = 0, 1, 2, 3
+POLICY_NAMES = {WAIT: "wait", NESTED: "nested", FCFS: "fcfs", FCFS_ONGOING: "fcfs_ongoing"}
 
 
 def fixed(v: int) -> Table:
