@@ -61,8 +61,8 @@ struct DevParams {
 // shared-memory bytes per warp for a given resident capacity / class count
 inline uint32_t warp_smem_bytes(uint32_t Rc, int K) {
   uint32_t b = Rc * 16u;                    // residents: a (i64) + packed (l, l', s, meta)
-  b += (uint32_t)K * (32u * 8u);            // visibility windows (t)
-  b += (uint32_t)K * (32u * 12u);           // admission windows (t, l, l')
+  b += (uint32_t)K * (32u * 12u);           // generated windows (t, l, l')
+  b += (uint32_t)K * (32u * 12u);           // private admission windows (t, l, l')
   b += 32u * 8u;                            // staged restart ticks
   b += (64u + 32u + 32u) * 4u + 16u;        // counters, rank cursors, snapshot, align
   b += 256u;                                // WarpStats (metric accumulators)

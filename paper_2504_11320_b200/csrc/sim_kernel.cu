@@ -164,10 +164,11 @@ struct WarpSim {
   // shared-memory views (this warp's slice)
   int64_t* ra;                       // [Rc] arrival tick of each resident
   uint64_t* rq;                      // [Rc] packed (l, l', s, meta)
-  int64_t* vt;                       // [K][32] visibility windows
-  int64_t* at;                       // [K][32] admission windows (t)
+  int64_t* vt;                       // [K][32] generated window (t): visibility + admission
+  uint16_t* vl; uint16_t* vlp;       // [K][32] generated window (l, l')
+  int64_t* at;                       // [K][32] private admission windows (t)
+  uint16_t* al; uint16_t* alp;       // [K][32] private admission windows (l, l')
   int64_t* re;                       // [32] staged restart-ring eviction ticks
-  uint16_t* al; uint16_t* alp;       // [K][32] admission windows (l, l')
   uint32_t* cnt;                     // [64] WAIT: residents per class; NESTED: [k] / [32+k]
   uint32_t* rank;                    // [32] NESTED per-segment rank cursors
   uint32_t* snap;                    // [32] NESTED entry counts at decision time
@@ -175,9 +176,13 @@ struct WarpSim {
   size_t ring_base;                  // first ring entry of this warp slot
 
   // per-class cursor state, lane c holds class c (and ring c for WAIT; ring 0
-  // otherwise).  vbase/abase: first arrival index held by the window;
-  // vprev/aprev: tick of arrival (base - 1), the scan carry.
-  uint32_t k_vis, vbase, k_adm, abase, rhead, rtail;
+  // otherwise).  The generated window [vbase, vbase+32) serves visibility
+  // and, while the backlog fits in it, admission too ("attached":
+  // k_adm >= vbase).  Pending arrivals still needed when the window advances
+  // are copied to the private window [abase, abase+pcount); a deeper backlog
+  // regenerates the private window from the Philox counter.  vprev/aprev:
+  // tick of arrival (base - 1), the scan carry.
+  uint32_t k_vis, vbase, k_adm, abase, pcount, rhead, rtail;
   int64_t vprev, aprev;
   uint32_t sv_k, sv_rhead;           // saved admission cursor (drop/rewind)
   int64_t sv_prev;
@@ -205,7 +210,9 @@ struct WarpSim {
     re = at + p.K * 32;
     al = (uint16_t*)(re + 32);
     alp = al + p.K * 32;
-    cnt = (uint32_t*)(((uintptr_t)(alp + p.K * 32) + 15) & ~(uintptr_t)15);
+    vl = alp + p.K * 32;
+    vlp = vl + p.K * 32;
+    cnt = (uint32_t*)(((uintptr_t)(vlp + p.K * 32) + 15) & ~(uintptr_t)15);
     rank = cnt + 64;
     snap = rank + 32;
     st = (WarpStats*)(snap + 32);
@@ -274,6 +281,17 @@ struct WarpSim {
   __device__ __forceinline__ uint32_t kadm(int c) const { return bcast32(k_adm, c); }
   __device__ __forceinline__ uint32_t rcount(int q) const { return bcast32(rtail, q) - bcast32(rhead, q); }
 
+  // tick of arrival k-1 of class c (k within the generated or private window)
+  __device__ int64_t t_before(int c, uint32_t k) const {
+    if (k == 0) return 0;
+    const uint32_t vb = bcast32(vbase, c);
+    if (k > vb) return vt[c * 32 + (k - 1 - vb)];
+    if (k == vb) return bcast64(vprev, c);
+    const uint32_t ab = bcast32(abase, c);
+    if (k > ab) return at[c * 32 + (k - 1 - ab)];
+    return bcast64(aprev, c);
+  }
+
   // ------------------------------------------------------ S2 ingestion
   // INGEST (DESIGN.md §4.4 step 1): arrivals with t <= now and t < T become
   // visible (join their FIFO).  Cursor only: count + arrival-time sum.
@@ -282,8 +300,22 @@ struct WarpSim {
       for (;;) {
         uint32_t kv = kvis(c), vb = bcast32(vbase, c);
         if (kv == vb + 32) {
+          const uint32_t ka = kadm(c);
+          if (ka >= vb && ka < vb + 32) {
+            // pending arrivals of the old window move to the private window
+            const uint32_t n = vb + 32 - ka, off = ka - vb;
+            const int64_t prev = t_before(c, ka);
+            __syncwarp();
+            if ((uint32_t)lane < n) {
+              at[c * 32 + lane] = vt[c * 32 + off + lane];
+              al[c * 32 + lane] = vl[c * 32 + off + lane];
+              alp[c * 32 + lane] = vlp[c * 32 + off + lane];
+            }
+            __syncwarp();
+            if (lane == c) { abase = ka; aprev = prev; pcount = n; }
+          }
           const int64_t carry = vt[c * 32 + 31];
-          fill<false>(c, kv, carry, vt, nullptr, nullptr);
+          fill<true>(c, kv, carry, vt, vl, vlp);
           if (lane == c) { vbase = kv; vprev = carry; }
           vb = kv;
         }
@@ -332,22 +364,38 @@ struct WarpSim {
     const int c_lo = POL == SCHED_WAIT ? q : 0;
     const int c_hi = POL == SCHED_WAIT ? q + 1 : P.K;
     while (want > 0) {
-      // (1) align class windows so each holds min(pending, 32) from k_adm
-      uint32_t my_j = 0, my_n = 0, total = 0;
+      // (1) each class's candidate window = its first min(pending, 32)
+      // waiting arrivals, as up to two sorted segments: private window part
+      // (or the generated window when attached) + the generated window
+      // continuing it.  Lane c keeps class c's descriptor.
+      uint32_t my_o1 = 0, my_n1 = 0, my_n2 = 0, my_priv = 0, my_n = 0, total = 0;
       for (int c = c_lo; c < c_hi; ++c) {
         const uint32_t ka = kadm(c);
         const uint32_t p = kvis(c) - ka;
         if (p == 0) continue;
-        uint32_t j = ka - bcast32(abase, c);
-        if (j == 32 || (j > 0 && p > 32 - j)) {
-          const int64_t prev = j > 0 ? at[c * 32 + j - 1] : bcast64(aprev, c);
-          fill<true>(c, ka, prev, at, al, alp);
-          if (lane == c) { abase = ka; aprev = prev; }
-          j = 0;
+        const uint32_t vb = bcast32(vbase, c);
+        uint32_t o1, n1, n2 = 0, priv = 0;
+        if (ka >= vb) {
+          o1 = ka - vb;
+          n1 = p;  // k_vis <= vbase + 32
+        } else {
+          priv = 1;
+          const uint32_t ab = bcast32(abase, c), pc = bcast32(pcount, c);
+          o1 = ka - ab;
+          n1 = min(p, pc - o1);
+          if (n1 < p && ab + pc == vb) n2 = min(p - n1, 32u - n1);
+          if (n1 + n2 < min(p, 32u)) {
+            // backlog deeper than the windows: regenerate the private window
+            const int64_t prev = t_before(c, ka);
+            fill<true>(c, ka, prev, at, al, alp);
+            if (lane == c) { abase = ka; aprev = prev; pcount = 32; }
+            o1 = 0;
+            n1 = min(p, 32u);
+            n2 = 0;
+          }
         }
-        const uint32_t n = min(p, 32u - j);
-        if (lane == c) { my_j = j; my_n = n; }
-        total += n;
+        if (lane == c) { my_o1 = o1; my_n1 = n1; my_n2 = n2; my_priv = priv; my_n = n1 + n2; }
+        total += n1 + n2;
       }
       const uint32_t nr = min(rcount(q), 32u);
       const uint32_t h0 = bcast32(rhead, q);
@@ -376,13 +424,24 @@ struct WarpSim {
           acc += n;
         }
         if (src == 32) pos = g - acc;
-        const uint32_t jsrc = __shfl_sync(FULL, my_j, src & 31);
+        const uint32_t s_o1 = __shfl_sync(FULL, my_o1, src & 31);
+        const uint32_t s_n1 = __shfl_sync(FULL, my_n1, src & 31);
+        const uint32_t s_priv = __shfl_sync(FULL, my_priv, src & 31);
         int64_t key = 0, a = 0;
         uint32_t l = 0, lp = 0, meta = 0, r = pos;
         if (act) {
           if (src < 32) {
-            const int idx = src * 32 + (int)(jsrc + pos);
-            key = at[idx]; a = key; l = al[idx]; lp = alp[idx]; meta = (uint32_t)src;
+            int idx;
+            const int64_t* tt;
+            const uint16_t *ll, *llp;
+            if (pos < s_n1) {
+              idx = src * 32 + (int)(s_o1 + pos);
+              tt = s_priv ? at : vt; ll = s_priv ? al : vl; llp = s_priv ? alp : vlp;
+            } else {
+              idx = src * 32 + (int)(pos - s_n1);
+              tt = vt; ll = vl; llp = vlp;
+            }
+            key = tt[idx]; a = key; l = ll[idx]; lp = llp[idx]; meta = (uint32_t)src;
             r += count_before(re, nr, key, false);       // restarts with e < t
           } else {
             key = re[pos];
@@ -396,9 +455,14 @@ struct WarpSim {
         for (int c = c_lo; c < c_hi; ++c) {
           const uint32_t n = bcast32(my_n, c);
           if (n == 0) continue;
-          const uint32_t jj = bcast32(my_j, c);
-          if (act && c != src)  // arrivals of class c before this candidate
-            r += count_before(at + c * 32 + jj, n, key, src == 32 || c < src);
+          const uint32_t n1 = bcast32(my_n1, c), o1 = bcast32(my_o1, c);
+          const int64_t* seg1 = (bcast32(my_priv, c) ? at : vt) + c * 32 + o1;
+          if (act && c != src) {  // arrivals of class c before this candidate
+            const bool le = src == 32 || c < src;
+            uint32_t k = count_before(seg1, n1, key, le);
+            if (k == n1 && n > n1) k += count_before(vt + c * 32, n - n1, key, le);
+            r += k;
+          }
         }
         if (act && r < m) {
           ra[base + r] = a;
@@ -448,19 +512,23 @@ struct WarpSim {
   __device__ void save_cursors() {
     sv_k = k_adm;
     sv_rhead = rhead;
-    sv_prev = aprev;
-    const uint32_t j = k_adm - abase;  // lane-local (own class)
-    if (lane < P.K && j > 0 && j <= 32) sv_prev = at[lane * 32 + j - 1];
+    sv_prev = 0;
+    if (lane < P.K && k_adm > 0) {  // tick of arrival k_adm - 1 of class `lane`
+      if (k_adm > vbase) sv_prev = vt[lane * 32 + (k_adm - 1 - vbase)];
+      else if (k_adm == vbase) sv_prev = vprev;
+      else if (k_adm > abase) sv_prev = at[lane * 32 + (k_adm - 1 - abase)];
+      else sv_prev = aprev;
+    }
     newc = 0;
   }
   __device__ void restore_cursors() {
     for (int c = 0; c < P.K; ++c) {
       const uint32_t k = bcast32(sv_k, c);
       const int64_t pv = bcast64(sv_prev, c);
-      const uint32_t ab = bcast32(abase, c);
-      if (!(k >= ab && k <= ab + 32)) {
+      const uint32_t ab = bcast32(abase, c), pc = bcast32(pcount, c);
+      if (k < bcast32(vbase, c) && !(k >= ab && k <= ab + pc)) {
         fill<true>(c, k, pv, at, al, alp);
-        if (lane == c) { abase = k; aprev = pv; }
+        if (lane == c) { abase = k; aprev = pv; pcount = 32; }
       }
       if (lane == c) k_adm = k;
     }
@@ -758,12 +826,11 @@ struct WarpSim {
       *st = z;
     }
     __syncwarp();
-    k_vis = vbase = k_adm = abase = rhead = rtail = 0;
+    k_vis = vbase = k_adm = abase = pcount = rhead = rtail = 0;
     vprev = aprev = 0;
     newc = 0;
     for (int c = 0; c < P.K; ++c) {
-      fill<false>(c, 0, 0, vt, nullptr, nullptr);
-      fill<true>(c, 0, 0, at, al, alp);
+      fill<true>(c, 0, 0, vt, vl, vlp);
     }
     cnt[lane] = 0;
     cnt[32 + lane] = 0;
