@@ -102,6 +102,15 @@ typedef struct {
   uint32_t tok_budget;        /* FCFS*: max prefill tokens per iteration (0 = none) */
   uint32_t max_resident;      /* per-replication resident capacity (0 = derive) */
   uint32_t restart_cap;       /* per-FIFO restart ring capacity (0 = default 8192) */
+  /* optional time-varying rates ("Time-Varying Arrival
+   * Rates"; NULL rf_off = all homogeneous): class c has pieces
+   * [rf_off[c], rf_off[c+1]) of (rf_t start second, rf_rate rate >= 0) with
+   * rf_t[first] = 0 and increasing starts, at most 32 pieces; an empty slice
+   * keeps the constant lambda[c].  Generated by exact time change
+   * (DESIGN.md §4.8); lambda[c] is still what sched_thresholds uses. */
+  const uint32_t* rf_off;     /* host [K+1] */
+  const double* rf_t;
+  const double* rf_rate;
   uint32_t spec_resident;     /* speculative capacity of the main launch (0 = derive);
                                  replications exceeding it are re-run with the safe
                                  capacity by a fallback launch on the same stream */
@@ -138,6 +147,13 @@ typedef struct {
   int32_t mem_exceeds_M;                  /* M^pi > M: LIFO-eviction regime */
   double p[32], theta[32], theta_lb[32];  /* NESTED: p_k, theta_k, 8 D / n_{k-1} (0 if n/a) */
   double budget_base, budget_queue, budget_hp, budget_total;
+  /* time-varying check (NESTED with rate pieces; Eq. nested_wait_thresholds_
+   * time_varying): sup_t of the arrivals accumulated in
+   * [t, t + dT_n] (must be < n_1), sup p_k over all windows (n_{k+1}/n_k must
+   * exceed it), and the verdict; tv_feasible = -1 when not applicable */
+  double tv_Lambda_pi;
+  double tv_p_star[32];
+  int32_t tv_feasible;
 } sched_threshold_report;
 
 int sched_thresholds(sched_t h, int32_t mode, double delta, double budget_B,

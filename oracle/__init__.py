@@ -55,6 +55,8 @@ class _Cfg(C.Structure):
         ("policy", C.c_int32), ("n_thr", C.c_int32), ("thr", C.POINTER(C.c_uint32)),
         ("n_seg", C.c_int32), ("seg_end", C.POINTER(C.c_uint16)),
         ("B", C.c_uint32), ("tok_budget", C.c_uint32), ("horizon_s", C.c_double),
+        ("rf_off", C.POINTER(C.c_int32)), ("rf_t", C.POINTER(C.c_double)),
+        ("rf_rate", C.POINTER(C.c_double)),
     ]
 
 
@@ -123,6 +125,19 @@ class Config:
         cfg.seg_end, cfg.n_seg = p, len(seg)
         cfg.B, cfg.tok_budget = policy.B, policy.tok_budget
         cfg.horizon_s = wl.horizon_s if horizon_s is None else horizon_s
+        rfs = getattr(wl, "rate_fn", None)
+        if rfs:
+            off, ts, rs = [0], [], []
+            for pieces in rfs:
+                for t0, r in (pieces or []):
+                    ts.append(t0)
+                    rs.append(r)
+                off.append(len(ts))
+            for name, data, dt in [("rf_off", off, np.int32), ("rf_t", ts or [0.0], np.float64),
+                                   ("rf_rate", rs or [0.0], np.float64)]:
+                a, p = _arr(data, dt)
+                keep.append(a)
+                setattr(cfg, name, p)
         self.cfg, self._keep = cfg, keep
 
 

@@ -137,8 +137,37 @@ uint64_t mix64(uint64_t z) {  // splitmix64 finaliser
   return z;
 }
 
+// Piecewise-constant rate function of one class, generated by time change
+// (DESIGN.md §4.8): operational time tau counts expected arrivals in units
+// of 2^-32; arrival k sits at tau_k = sum of (int64)(E_i * 2^32); its tick
+// is the inverse of the integrated rate Lambda(t), piece by piece.
+struct RatePieces {
+  std::vector<int64_t> B;      // piece start ticks
+  std::vector<int64_t> Lam;    // integrated rate at piece starts (operational ticks)
+  std::vector<double> lam;     // rate of each piece
+  bool empty() const { return B.empty(); }
+  void build(const double* t, const double* r, int n) {
+    for (int p = 0; p < n; ++p) { B.push_back(std::llround(t[p] * 1e12)); lam.push_back(r[p]); }
+    Lam.push_back(0);
+    for (int p = 0; p + 1 < n; ++p)
+      Lam.push_back(Lam[p] + (int64_t)(((lam[p] * (double)(B[p + 1] - B[p])) * 4294967296.0) / 1e12));
+  }
+  // arrival tick at operational time tau (INT64_MAX: no more arrivals)
+  int64_t tick(int64_t tau) const {
+    int p = 0;
+    for (int q = 1; q < (int)B.size(); ++q)
+      if (Lam[q] <= tau) p = q;
+    if (lam[p] == 0.0) return INT64_MAX;  // only the last piece can be reached with rate 0
+    const double scale = 1e12 / (lam[p] * 4294967296.0);
+    int64_t t = B[p] + (int64_t)((double)(tau - Lam[p]) * scale);
+    if (p + 1 < (int)B.size()) t = std::min(t, B[p + 1] - 1);
+    return t;
+  }
+};
+
 struct Setup {  // per-config constants, recomputed here from the raw config
   int K, policy;
+  std::vector<RatePieces> rf;      // time-varying classes (empty = homogeneous)
   std::vector<double> gap_scale;   // 1e12 / lambda_c, ticks per unit exponential
   std::vector<LenTable> ltab, lptab;
   int64_t d0_t, d1_t, T_t, M;
@@ -153,6 +182,10 @@ struct Setup {  // per-config constants, recomputed here from the raw config
       a.build(cfg->l_val + cfg->l_off[c], cfg->l_w + cfg->l_off[c], cfg->l_off[c + 1] - cfg->l_off[c]);
       b.build(cfg->lp_val + cfg->lp_off[c], cfg->lp_w + cfg->lp_off[c], cfg->lp_off[c + 1] - cfg->lp_off[c]);
       ltab.push_back(a); lptab.push_back(b);
+      RatePieces pc;
+      if (cfg->rf_off && cfg->rf_off[c + 1] > cfg->rf_off[c])
+        pc.build(cfg->rf_t + cfg->rf_off[c], cfg->rf_rate + cfg->rf_off[c], cfg->rf_off[c + 1] - cfg->rf_off[c]);
+      rf.push_back(pc);
     }
     // 1 tick = 1 ps
     d0_t = std::llround(cfg->d0_s * 1e12);
@@ -171,6 +204,7 @@ struct Setup {  // per-config constants, recomputed here from the raw config
 struct ArrivalStream {
   const Setup* S; uint64_t seed; uint32_t r; int c;
   uint32_t k = 0; int64_t t = 0;  // next arrival: index k, tick t
+  int64_t tau = 0, tau_prev = 0;  // operational time (time-varying classes)
   int l = 0, lp = 0;
   bool exhausted = false;         // lambda = 0
   // explicit-trace mode
@@ -185,18 +219,26 @@ struct ArrivalStream {
       t = tr_t[i]; l = tr_l[i]; lp = tr_lp[i];
       return;
     }
-    if (S->gap_scale[c] == 0.0) { exhausted = true; return; }
+    const bool tv = !S->rf[c].empty();
+    if (!tv && S->gap_scale[c] == 0.0) { exhausted = true; return; }
     uint32_t ctr[4] = {k, r, (uint32_t)c, 0u};
     uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
     uint32_t x[4];
     philox(ctr, key, x);
     double E = exp_from_bits(x[0], x[1]);
-    int64_t gap = (int64_t)(E * S->gap_scale[c]);  // truncation toward zero
-    t = t_prev + gap;
+    if (tv) {
+      // time change: tau_k = tau_{k-1} + (int64)(E * 2^32), t_k = Lambda^{-1}(tau_k)
+      tau = tau_prev + (int64_t)(E * 4294967296.0);
+      t = S->rf[c].tick(tau);
+      if (t == INT64_MAX) { exhausted = true; return; }
+    } else {
+      int64_t gap = (int64_t)(E * S->gap_scale[c]);  // truncation toward zero
+      t = t_prev + gap;
+    }
     l = S->ltab[c].sample(x[2]);
     lp = S->lptab[c].sample(x[3]);
   }
-  void advance() { t_prev = t; ++k; ++tr_pos; draw(); }
+  void advance() { t_prev = t; tau_prev = tau; ++k; ++tr_pos; draw(); }
 };
 
 struct Plan {

@@ -231,3 +231,52 @@ def thm2_budget(wl, seg_end, n, B: float, delta: float):
             th = theta(n[k - 1], n[k], p)
             hp += foot * math.log((L - 1) * B / delta) / th
     return base, queue, hp, base + queue + hp
+
+
+# ------------------------------------------------------- time-varying rates
+def accumulated(rate_pieces, lam_const, t0: Fr, t1: Fr) -> Fr:
+    """lambda_j[t0, t1] = int_{t0}^{t1} lambda_j(s) ds for a piecewise-constant
+    rate (PAPER.md:1888, "accumulated arrivals of type j")."""
+    if not rate_pieces:
+        return Fr(lam_const) * (t1 - t0)
+    acc = Fr(0)
+    for p, (b, r) in enumerate(rate_pieces):
+        lo = max(t0, Fr(b))
+        hi = t1 if p + 1 == len(rate_pieces) else min(t1, Fr(rate_pieces[p + 1][0]))
+        if hi > lo:
+            acc += Fr(r) * (hi - lo)
+    return acc
+
+
+def validate_time_varying(wl, seg_end, n, dT):
+    """Eq. nested_wait_thresholds_time_varying (PAPER.md:1898-1906) for
+    piecewise-constant rates: Lambda^pi = sup_t sum_j lambda_j[t, t+dT] must
+    be < n_1 and n_{k+1}/n_k > sup_{t,dt} p_k[t, t+dt].  The window integral
+    is piecewise linear in t (sup at t = b or b - dT); p_k over a window is a
+    mediant of instantaneous ratios, so its sup is the largest per-piece
+    ratio.  Returns (Lambda_pi, [p*_k for k>=1], feasible)."""
+    dT = Fr(dT)
+    rfs = wl.rate_fn or [None] * wl.K
+    cand = {Fr(0)}
+    for pieces in rfs:
+        for b, _ in (pieces or []):
+            cand.add(Fr(b))
+            cand.add(max(Fr(0), Fr(b) - dT))
+    sup = max(sum(accumulated(rfs[c], wl.lam[c], t, t + dT) for c in range(wl.K)) for t in cand)
+    pstar = [Fr(0)]
+    for k in range(1, len(seg_end)):
+        lo, lo1 = (0 if k == 1 else seg_end[k - 2]), seg_end[k - 1]
+        best = Fr(0)
+        for t in cand:
+            tk = tk1 = Fr(0)
+            for c in range(wl.K):
+                pieces = rfs[c]
+                r = Fr(wl.lam[c]) if not pieces else Fr([rr for b, rr in pieces if Fr(b) <= t][-1])
+                W = sum(w for _, w in wl.lp_tab[c])
+                tk += r * Fr(sum(w for v, w in wl.lp_tab[c] if v > lo), W)
+                tk1 += r * Fr(sum(w for v, w in wl.lp_tab[c] if v > lo1), W)
+            if tk > 0:
+                best = max(best, tk1 / tk)
+        pstar.append(best)
+    ok = sup < n[0] and all(Fr(n[k]) > Fr(n[k - 1]) * pstar[k] for k in range(1, len(seg_end)))
+    return sup, pstar, ok

@@ -45,6 +45,12 @@ typedef struct {
   uint32_t B;                /* FCFS: max resident prompts */
   uint32_t tok_budget;       /* FCFS: prefill tokens per iteration, 0 = inf */
   double horizon_s;          /* T */
+  /* time-varying rates (optional, NULL = homogeneous): class c has pieces
+   * [rf_off[c], rf_off[c+1]) of (start second, rate); an empty slice means
+   * the constant rate lam[c]; the first start must be 0 */
+  const int32_t* rf_off;
+  const double* rf_t;
+  const double* rf_rate;
 } orc_config;
 
 /* Philox4x32-10 (Salmon et al. SC'11). */

@@ -51,7 +51,10 @@ class SchedConfig(C.Structure):
         ("policy", C.c_int32), ("n_thr", C.c_uint32), ("thresholds", C.POINTER(C.c_uint32)),
         ("n_seg", C.c_uint32), ("seg_end", C.POINTER(C.c_uint16)),
         ("B", C.c_uint32), ("tok_budget", C.c_uint32), ("max_resident", C.c_uint32),
-        ("restart_cap", C.c_uint32), ("spec_resident", C.c_uint32), ("device", C.c_int32),
+        ("restart_cap", C.c_uint32),
+        ("rf_off", C.POINTER(C.c_uint32)), ("rf_t", C.POINTER(C.c_double)),
+        ("rf_rate", C.POINTER(C.c_double)),
+        ("spec_resident", C.c_uint32), ("device", C.c_int32),
     ]
 
 
@@ -65,6 +68,7 @@ class ThresholdReport(C.Structure):
         ("p", C.c_double * 32), ("theta", C.c_double * 32), ("theta_lb", C.c_double * 32),
         ("budget_base", C.c_double), ("budget_queue", C.c_double),
         ("budget_hp", C.c_double), ("budget_total", C.c_double),
+        ("tv_Lambda_pi", C.c_double), ("tv_p_star", C.c_double * 32), ("tv_feasible", C.c_int32),
     ]
 
 
@@ -162,6 +166,19 @@ class Scheduler:
         cfg.B, cfg.tok_budget = policy.B, policy.tok_budget
         cfg.max_resident, cfg.restart_cap, cfg.device = max_resident, restart_cap, device
         cfg.spec_resident = spec_resident
+        rfs = getattr(workload, "rate_fn", None)
+        if rfs:
+            off, ts, rs = [0], [], []
+            for pieces in rfs:
+                for t0, r in (pieces or []):
+                    ts.append(t0)
+                    rs.append(r)
+                off.append(len(ts))
+            for name, data, dt in [("rf_off", off, np.uint32), ("rf_t", ts or [0.0], np.float64),
+                                   ("rf_rate", rs or [0.0], np.float64)]:
+                a, p = _arr(data, dt)
+                keep.append(a)
+                setattr(cfg, name, p)
         h = C.c_void_p()
         _check(lib().sched_create(C.byref(h), C.byref(cfg)))
         self._h = h
@@ -191,7 +208,8 @@ class Scheduler:
                     mem_exceeds_M=bool(rep.mem_exceeds_M), p=list(rep.p[:n]),
                     theta=list(rep.theta[:n]), theta_lb=list(rep.theta_lb[:n]),
                     budget=(rep.budget_base, rep.budget_queue, rep.budget_hp, rep.budget_total),
-                    status=rc)
+                    tv_Lambda_pi=rep.tv_Lambda_pi, tv_p_star=list(rep.tv_p_star[:n]),
+                    tv_feasible=rep.tv_feasible, status=rc)
 
     def launch_info(self) -> dict:
         li = LaunchInfo()

@@ -47,6 +47,12 @@ struct sched_s {
   std::vector<uint64_t> h_cdf_thr;     // uploaded lazily by prepare()
   std::vector<uint16_t> h_cdf_val;
   std::vector<uint8_t> h_stage_info;
+  std::vector<int64_t> h_rf_B, h_rf_Lam;   // time-varying rate pieces
+  std::vector<double> h_rf_scale;
+  int64_t* d_rf_B = nullptr;
+  int64_t* d_rf_Lam = nullptr;
+  double* d_rf_scale = nullptr;
+  bool tv_any = false;
   // scratch
   int64_t* d_ring_a = nullptr;
   int64_t* d_ring_e = nullptr;
@@ -144,6 +150,19 @@ int prepare(sched_s* h) {
     h->base.cdf_thr = h->d_cdf_thr;
     h->base.cdf_val = h->d_cdf_val;
     h->base.stage_info = h->d_stage_info;
+    h->base.tv_any = h->tv_any ? 1 : 0;
+    if (h->tv_any) {
+      const size_t n = h->h_rf_B.size();
+      CK(cudaMalloc(&h->d_rf_B, n * 8));
+      CK(cudaMalloc(&h->d_rf_Lam, n * 8));
+      CK(cudaMalloc(&h->d_rf_scale, n * 8));
+      CK(cudaMemcpy(h->d_rf_B, h->h_rf_B.data(), n * 8, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(h->d_rf_Lam, h->h_rf_Lam.data(), n * 8, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(h->d_rf_scale, h->h_rf_scale.data(), n * 8, cudaMemcpyHostToDevice));
+      h->base.rf_B = h->d_rf_B;
+      h->base.rf_Lam = h->d_rf_Lam;
+      h->base.rf_scale = h->d_rf_scale;
+    }
   }
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, h->device));
@@ -164,7 +183,7 @@ int prepare(sched_s* h) {
   h->fallback = h->Rc < h->Rc_safe;
   // choose warps per block maximising resident warps per SM
   auto size_launch = [&](uint32_t Rc, uint32_t* wsm, int* wpb_out, int* bps_out) -> int {
-    *wsm = warp_smem_bytes(Rc, K);
+    *wsm = warp_smem_bytes(Rc, K, h->tv_any);
     int best_w = 0;
     const int cands[] = {8, 4, 2, 1};
     for (int wpb : cands) {
@@ -328,6 +347,38 @@ int sched_create(sched_t* out, const sched_config* cfg) {
       }
     }
     h->base.cls[c].gap_scale = cfg->lambda[c] > 0 ? 1e12 / cfg->lambda[c] : 0.0;
+    // time-varying pieces: start ticks, integrated rate (2^-32 expected
+    // arrivals), inverse-rate tick scale
+    std::vector<std::pair<double, double>> pieces;
+    if (cfg->rf_off && cfg->rf_off[c + 1] > cfg->rf_off[c]) {
+      const uint32_t a = cfg->rf_off[c], b = cfg->rf_off[c + 1];
+      if (!cfg->rf_t || !cfg->rf_rate || b - a > 32 || cfg->rf_t[a] != 0.0) {
+        delete h;
+        return fail(SCHED_E_INVALID, "rate pieces: need rf_t/rf_rate, <= 32 pieces, first start 0");
+      }
+      h->base.cls[c].rf_off = (uint32_t)h->h_rf_B.size();
+      h->base.cls[c].rf_n = b - a;
+      int64_t Lam = 0;
+      for (uint32_t i = a; i < b; ++i) {
+        const double r = cfg->rf_rate[i];
+        if (!(r >= 0) || std::isinf(r) || (i > a && !(cfg->rf_t[i] > cfg->rf_t[i - 1]))) {
+          delete h;
+          return fail(SCHED_E_INVALID, "rate pieces: rates >= 0, increasing starts");
+        }
+        const int64_t B = std::llround(cfg->rf_t[i] * 1e12);
+        if (i > a) {
+          const int64_t Bp = h->h_rf_B.back();
+          const double rp = cfg->rf_rate[i - 1];
+          Lam += (int64_t)(((rp * (double)(B - Bp)) * 4294967296.0) / 1e12);
+        }
+        h->h_rf_B.push_back(B);
+        h->h_rf_Lam.push_back(Lam);
+        h->h_rf_scale.push_back(r > 0 ? 1e12 / (r * 4294967296.0) : 0.0);
+        pieces.push_back({cfg->rf_t[i], r});
+      }
+      h->tv_any = true;
+    }
+    in.rf.push_back(pieces);
   }
   h->max_lp = max_lp;
   h->min_l = min_l;
@@ -554,6 +605,9 @@ void sched_destroy(sched_t h) {
   cudaFree(h->d_counter);
   cudaFree(h->d_out);
   cudaFree(h->d_retry);
+  cudaFree(h->d_rf_B);
+  cudaFree(h->d_rf_Lam);
+  cudaFree(h->d_rf_scale);
   delete h;
 }
 

@@ -372,6 +372,69 @@ int compute_thresholds(const SetupInput& in, int mode, double delta, double budg
   } else {
     n.clear();  // FCFS has no thresholds
   }
+  // time-varying check, NESTED only.  For piecewise-
+  // constant rates the accumulated arrivals over [t, t+dT] are piecewise
+  // linear in t, so the supremum is attained at t = b_p or t = b_p - dT;
+  // p_k over any window is a mediant of per-piece ratios, so its supremum
+  // is the largest per-piece ratio.
+  out->tv_feasible = -1;
+  bool any_tv = false;
+  for (auto& r : in.rf) any_tv = any_tv || !r.empty();
+  if (any_tv && in.policy == 1 && !n.empty()) {
+    const double dT = out->dT_n;
+    auto rate_at = [&](int c, double t) {  // lambda_c(t)
+      if (in.rf[c].empty()) return in.lambda[c];
+      double r = 0;
+      for (auto& pc : in.rf[c]) if (pc.first <= t) r = pc.second;
+      return r;
+    };
+    auto integral = [&](int c, double t0, double t1) {  // int_t0^t1 lambda_c
+      if (in.rf[c].empty()) return in.lambda[c] * (t1 - t0);
+      double acc = 0;
+      const auto& P = in.rf[c];
+      for (size_t p = 0; p < P.size(); ++p) {
+        const double a = std::max(t0, P[p].first);
+        const double b = std::min(t1, p + 1 < P.size() ? P[p + 1].first : 1e300);
+        if (b > a) acc += P[p].second * (b - a);
+      }
+      return acc;
+    };
+    std::vector<double> cand{0.0};
+    for (auto& r : in.rf)
+      for (auto& pc : r) { cand.push_back(pc.first); cand.push_back(std::max(0.0, pc.first - dT)); }
+    double sup = 0;
+    for (double t : cand) {
+      double a = 0;
+      for (int c = 0; c < K; ++c) a += integral(c, t, t + dT);
+      sup = std::max(sup, a);
+    }
+    out->tv_Lambda_pi = sup;
+    bool ok = sup < (double)n[0];
+    const int L = (int)in.seg_end.size();
+    for (int k = 0; k + 1 < L; ++k) {
+      // per-piece tail rates of segments k and k+1
+      double pmax = 0;
+      for (double t : cand) {
+        double tk = 0, tk1 = 0;
+        const uint64_t lo = k == 0 ? 0 : in.seg_end[k - 1], lo1 = in.seg_end[k];
+        for (int c = 0; c < K; ++c) {
+          double W = 0, w0 = 0, w1 = 0;
+          for (auto& e : in.lp[c]) {
+            W += (double)e.second;
+            if (e.first > lo) w0 += (double)e.second;
+            if (e.first > lo1) w1 += (double)e.second;
+          }
+          const double r = rate_at(c, t);
+          tk += r * w0 / W;
+          tk1 += r * w1 / W;
+        }
+        if (tk > 0) pmax = std::max(pmax, tk1 / tk);
+      }
+      if (k + 1 < 32) out->tv_p_star[k + 1] = pmax;
+      if (!((double)n[k + 1] > (double)n[k] * pmax)) ok = false;
+    }
+    out->tv_feasible = ok;
+  }
   out->n_thr = (uint32_t)std::min<size_t>(n.size(), 32);
   for (size_t i = 0; i < n.size() && i < 32; ++i) out->thresholds[i] = n[i];
   if (chosen) *chosen = n;

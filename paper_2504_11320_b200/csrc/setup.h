@@ -21,6 +21,7 @@ struct SetupInput {
   std::vector<uint32_t> thresholds;  // empty = choose
   std::vector<uint16_t> seg_end;
   uint32_t B;
+  std::vector<std::vector<std::pair<double, double>>> rf;  // per class (start s, rate); empty = constant
 };
 
 // returns 0, -2 (unstable; report filled), -3 (infeasible), -1 (invalid)

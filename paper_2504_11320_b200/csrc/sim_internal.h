@@ -13,6 +13,7 @@ struct ClassParam {
   double gap_scale;        // 1e12 / lambda (ticks per unit exponential); 0 = no arrivals
   uint32_t l_off, l_n;     // CDF table slice (thresholds u64 [n-1], values u16 [n])
   uint32_t lp_off, lp_n;
+  uint32_t rf_off, rf_n;   // time-varying rate pieces (rf_n = 0: homogeneous)
 };
 
 // Everything one launch needs, passed by value (lives in the constant bank).
@@ -35,6 +36,13 @@ struct DevParams {
   const uint64_t* cdf_thr; // device
   const uint16_t* cdf_val; // device
   const uint8_t* stage_info; // NESTED: stage -> segment | entry<<7 (device)
+  // time-varying classes: per piece start tick, integrated
+  // rate at the start (operational ticks, 2^-32 expected arrivals), tick
+  // scale 1e12 / (lambda 2^32) (0 = zero rate)
+  const int64_t* rf_B;
+  const int64_t* rf_Lam;
+  const double* rf_scale;
+  uint32_t tv_any;         // some class is time-varying: operational-time windows exist
   // explicit traces (trace_mode): per (rep, class) slices of t / l / lp
   const int64_t* tr_t;
   const uint16_t* tr_l;
@@ -59,13 +67,14 @@ struct DevParams {
 };
 
 // shared-memory bytes per warp for a given resident capacity / class count
-inline uint32_t warp_smem_bytes(uint32_t Rc, int K) {
+inline uint32_t warp_smem_bytes(uint32_t Rc, int K, bool tv = false) {
   uint32_t b = Rc * 16u;                    // residents: a (i64) + packed (l, l', s, meta)
   b += (uint32_t)K * (32u * 12u);           // generated windows (t, l, l')
   b += (uint32_t)K * (32u * 12u);           // private admission windows (t, l, l')
   b += 32u * 8u;                            // staged restart ticks
   b += (64u + 32u + 32u) * 4u + 16u;        // counters, rank cursors, snapshot, align
   b += 256u;                                // WarpStats (metric accumulators)
+  if (tv) b += (uint32_t)K * (32u * 16u);   // operational-time windows (generated, private)
   return (b + 15u) & ~15u;
 }
 

@@ -169,6 +169,7 @@ struct WarpSim {
   int64_t* at;                       // [K][32] private admission windows (t)
   uint16_t* al; uint16_t* alp;       // [K][32] private admission windows (l, l')
   int64_t* re;                       // [32] staged restart-ring eviction ticks
+  int64_t* vtau; int64_t* atau;      // [K][32] operational time (time-varying classes only)
   uint32_t* cnt;                     // [64] WAIT: residents per class; NESTED: [k] / [32+k]
   uint32_t* rank;                    // [32] NESTED per-segment rank cursors
   uint32_t* snap;                    // [32] NESTED entry counts at decision time
@@ -216,6 +217,8 @@ struct WarpSim {
     rank = cnt + 64;
     snap = rank + 32;
     st = (WarpStats*)(snap + 32);
+    vtau = (int64_t*)((unsigned char*)st + 256);
+    atau = vtau + p.K * 32;
   }
 
   __device__ void flush_acc() {
@@ -239,12 +242,32 @@ struct WarpSim {
   // Fill the 32 arrivals [base, base+32) of class c: lane i draws arrival
   // base+i from Philox counter (k, r, c, 0), gaps are
   // turned into ticks by an inclusive warp scan on top of `prev`.
+  __device__ __forceinline__ bool is_tv(int c) const { return !TRACE && P.cls[c].rf_n != 0; }
+
+  // arrival tick at operational time tau of a time-varying class: invert the
+  // integrated piecewise-constant rate
+  __device__ __forceinline__ int64_t tv_tick(int c, int64_t tau) const {
+    const uint32_t off = P.cls[c].rf_off, n = P.cls[c].rf_n;
+    uint32_t lo = 0, hi = n;  // largest p with Lam[p] <= tau (Lam[0] = 0)
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(P.rf_Lam + off + mid) <= tau) lo = mid; else hi = mid;
+    }
+    const double scale = __ldg(P.rf_scale + off + lo);
+    if (scale == 0.0) return TMAX;
+    int64_t t = __ldg(P.rf_B + off + lo) +
+                __double2ll_rz(__dmul_rn(__ll2double_rn(tau - __ldg(P.rf_Lam + off + lo)), scale));
+    if (lo + 1 < n) t = min(t, __ldg(P.rf_B + off + lo + 1) - 1);
+    return t;
+  }
+
   template <bool WITH_LEN>
   __device__ __forceinline__ void fill(int c, uint32_t base, int64_t prev, int64_t* wt,
                                        uint16_t* wl, uint16_t* wlp) {
     const uint32_t k = base + lane;
-    int64_t t;
+    int64_t t, tau = 0;
     uint32_t l = 1, lp = 1;
+    const bool tv = is_tv(c);
     if (TRACE) {
       const int64_t beg = P.tr_off[(size_t)rep * P.K + c];
       const int64_t end = P.tr_off[(size_t)rep * P.K + c + 1];
@@ -256,14 +279,21 @@ struct WarpSim {
       }
     } else {
       const double gs = P.cls[c].gap_scale;
-      if (gs == 0.0) {
+      if (gs == 0.0 && !tv) {
         t = TMAX;
       } else {
         uint32_t x0, x1, x2, x3;
         philox4x32_10(k, rglob, (uint32_t)c, 0u, (uint32_t)P.seed, (uint32_t)(P.seed >> 32),
                       x0, x1, x2, x3);
-        const int64_t gap = __double2ll_rz(__dmul_rn(neglog_bits(x0, x1), gs));
-        t = prev + warp_incl_scan_i64(gap, lane);
+        if (tv) {
+          // time change: tau_k = tau_{k-1} + (int64)(E 2^32), t_k = Lambda^{-1}(tau_k)
+          const int64_t g = __double2ll_rz(__dmul_rn(neglog_bits(x0, x1), 4294967296.0));
+          tau = prev + warp_incl_scan_i64(g, lane);
+          t = tv_tick(c, tau);
+        } else {
+          const int64_t gap = __double2ll_rz(__dmul_rn(neglog_bits(x0, x1), gs));
+          t = prev + warp_incl_scan_i64(gap, lane);
+        }
         if (WITH_LEN) {
           l = cdf_sample(P.cdf_thr, P.cdf_val, P.cls[c].l_off, P.cls[c].l_n, x2);
           lp = cdf_sample(P.cdf_thr, P.cdf_val, P.cls[c].lp_off, P.cls[c].lp_n, x3);
@@ -273,6 +303,7 @@ struct WarpSim {
     __syncwarp();
     wt[c * 32 + lane] = t;
     if (WITH_LEN) { wl[c * 32 + lane] = (uint16_t)l; wlp[c * 32 + lane] = (uint16_t)lp; }
+    if (tv) (wt == vt ? vtau : atau)[c * 32 + lane] = tau;
     __syncwarp();
   }
 
@@ -281,14 +312,16 @@ struct WarpSim {
   __device__ __forceinline__ uint32_t kadm(int c) const { return bcast32(k_adm, c); }
   __device__ __forceinline__ uint32_t rcount(int q) const { return bcast32(rtail, q) - bcast32(rhead, q); }
 
-  // tick of arrival k-1 of class c (k within the generated or private window)
-  __device__ int64_t t_before(int c, uint32_t k) const {
+  // scan carry of arrival k-1 of class c: its tick, or its operational time
+  // for a time-varying class (k within the generated or private window)
+  __device__ int64_t carry_before(int c, uint32_t k) const {
     if (k == 0) return 0;
+    const bool tv = is_tv(c);
     const uint32_t vb = bcast32(vbase, c);
-    if (k > vb) return vt[c * 32 + (k - 1 - vb)];
+    if (k > vb) return (tv ? vtau : vt)[c * 32 + (k - 1 - vb)];
     if (k == vb) return bcast64(vprev, c);
     const uint32_t ab = bcast32(abase, c);
-    if (k > ab) return at[c * 32 + (k - 1 - ab)];
+    if (k > ab) return (tv ? atau : at)[c * 32 + (k - 1 - ab)];
     return bcast64(aprev, c);
   }
 
@@ -304,17 +337,18 @@ struct WarpSim {
           if (ka >= vb && ka < vb + 32) {
             // pending arrivals of the old window move to the private window
             const uint32_t n = vb + 32 - ka, off = ka - vb;
-            const int64_t prev = t_before(c, ka);
+            const int64_t prev = carry_before(c, ka);
             __syncwarp();
             if ((uint32_t)lane < n) {
               at[c * 32 + lane] = vt[c * 32 + off + lane];
               al[c * 32 + lane] = vl[c * 32 + off + lane];
               alp[c * 32 + lane] = vlp[c * 32 + off + lane];
+              if (is_tv(c)) atau[c * 32 + lane] = vtau[c * 32 + off + lane];
             }
             __syncwarp();
             if (lane == c) { abase = ka; aprev = prev; pcount = n; }
           }
-          const int64_t carry = vt[c * 32 + 31];
+          const int64_t carry = (is_tv(c) ? vtau : vt)[c * 32 + 31];
           fill<true>(c, kv, carry, vt, vl, vlp);
           if (lane == c) { vbase = kv; vprev = carry; }
           vb = kv;
@@ -386,7 +420,7 @@ struct WarpSim {
           if (n1 < p && ab + pc == vb) n2 = min(p - n1, 32u - n1);
           if (n1 + n2 < min(p, 32u)) {
             // backlog deeper than the windows: regenerate the private window
-            const int64_t prev = t_before(c, ka);
+            const int64_t prev = carry_before(c, ka);
             fill<true>(c, ka, prev, at, al, alp);
             if (lane == c) { abase = ka; aprev = prev; pcount = 32; }
             o1 = 0;
@@ -513,10 +547,11 @@ struct WarpSim {
     sv_k = k_adm;
     sv_rhead = rhead;
     sv_prev = 0;
-    if (lane < P.K && k_adm > 0) {  // tick of arrival k_adm - 1 of class `lane`
-      if (k_adm > vbase) sv_prev = vt[lane * 32 + (k_adm - 1 - vbase)];
+    if (lane < P.K && k_adm > 0) {  // scan carry of arrival k_adm - 1 of class `lane`
+      const bool tv = is_tv(lane);
+      if (k_adm > vbase) sv_prev = (tv ? vtau : vt)[lane * 32 + (k_adm - 1 - vbase)];
       else if (k_adm == vbase) sv_prev = vprev;
-      else if (k_adm > abase) sv_prev = at[lane * 32 + (k_adm - 1 - abase)];
+      else if (k_adm > abase) sv_prev = (tv ? atau : at)[lane * 32 + (k_adm - 1 - abase)];
       else sv_prev = aprev;
     }
     newc = 0;

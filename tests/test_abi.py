@@ -136,3 +136,16 @@ def test_ctypes_struct_sizes_match_header():
                                os.path.join(d, "m"), os.path.join(d, "m.c")])
         sizes = [int(x) for x in subprocess.check_output([os.path.join(d, "m")]).split()]
     assert sizes == [C.sizeof(SchedConfig), C.sizeof(ThresholdReport), C.sizeof(LaunchInfo)]
+
+
+@pytest.mark.parametrize("n", [[7, 7, 7, 5], [11, 11, 10, 7]])
+def test_time_varying_check_matches_oracle(n):
+    seg = [20, 40, 80, 160]
+    wl = W.c3a_time_varying()
+    r = Scheduler(wl, W.Policy(W.NESTED, seg_end=seg), n).thresholds()
+    dT = fl.Fr(wl.d0_s) + fl.Fr(wl.d1_s) * fl.nested_memory_exact(wl, seg, n)
+    sup, pstar, ok = fl.validate_time_varying(wl, seg, n, dT)
+    assert r["dT_n"] == pytest.approx(float(dT), rel=1e-12)
+    assert r["tv_Lambda_pi"] == pytest.approx(float(sup), rel=1e-9)
+    assert r["tv_p_star"][1:] == pytest.approx([float(x) for x in pstar[1:]], rel=1e-12)
+    assert r["tv_feasible"] == int(ok)

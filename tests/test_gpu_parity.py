@@ -106,6 +106,34 @@ def test_c5_chat_shaped(qps):
     check(wl, W.Policy(W.FCFS_ONGOING, B=1024), [0], 8, horizon_s=120.0, **kw)
 
 
+# ------------------------------------------------ time-varying rates (NEXT 2)
+def test_c3a_time_varying_all_policies():
+    wl = W.c3a_time_varying()
+    check(wl, W.Policy(W.NESTED, seg_end=SEG3A), [11, 11, 10, 7], 16)
+    check(wl, W.Policy(W.NESTED, seg_end=SEG3A), [7, 7, 7, 5], 16)
+    check(wl, W.Policy(W.FCFS, B=1024), [0], 16)
+    check(wl, W.Policy(W.WAIT), [3, 5, 9, 17], 16)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_time_varying(seed):
+    rng = np.random.default_rng(500 + seed)
+    wl = W.random_small(rng, horizon_s=1.5)
+    rf = []
+    for c in range(wl.K):
+        if rng.random() < 0.3:
+            rf.append(None)
+            continue
+        npieces = int(rng.integers(1, 5))
+        starts = [0.0] + sorted(float(x) for x in rng.uniform(0.05, 1.4, npieces - 1))
+        rf.append([(t0, float(rng.choice([0.0, 10.0, 40.0, 150.0]))) for t0 in starts])
+    wl.rate_fn = rf
+    maxlp = max(v for t in wl.lp_tab for v, _ in t)
+    check(wl, W.Policy(W.WAIT), [int(rng.integers(1, 5)) for _ in range(wl.K)], 16)
+    check(wl, W.Policy(W.FCFS, B=int(rng.integers(1, 40))), [0], 16)
+    check(wl, W.Policy(W.NESTED, seg_end=[maxlp]), [int(rng.integers(1, 4))], 16)
+
+
 # ------------------------------------------------- random small systems
 @pytest.mark.parametrize("seed", range(40))
 def test_random_small_workloads(seed):

@@ -485,3 +485,61 @@ def test_littles_law_and_prop2_c2():
         thr_tok = rows[F["completed_tokens"]] / T
         se = thr_tok.std(ddof=1) / math.sqrt(len(thr_tok))
         assert thr_tok.mean() <= float(fl.fluid(W.C2).thr_star) + 3 * se
+
+
+# ---------------------------------------------- time-varying rates (NEXT 2)
+def test_time_varying_counts_follow_integrated_rate():
+    """Nonhomogeneous Poisson by time change: the number of
+    arrivals in each piece is Poisson with mean rate x duration, a zero-rate
+    piece has none, and arrivals are nondecreasing in time."""
+    pieces = [(0.0, 40.0), (5.0, 0.0), (7.5, 120.0), (10.0, 10.0)]
+    wl = W.Workload("tv", [40.0], [W.fixed(2)], [W.fixed(3)], M=100, horizon_s=20.0, seed=21)
+    wl.rate_fn = [pieces]
+    bounds = [0.0, 5.0, 7.5, 10.0, 20.0]
+    means = [40 * 5, 0, 120 * 2.5, 10 * 10]
+    counts = np.zeros((200, 4))
+    for r in range(200):
+        t, _, _ = oracle.gen_arrivals(wl, r, 0, 1200)
+        assert np.all(np.diff(t) >= 0)
+        for i in range(4):
+            counts[r, i] = np.sum((t >= bounds[i] * TPS) & (t < bounds[i + 1] * TPS))
+    assert counts[:, 1].sum() == 0
+    for i in (0, 2, 3):
+        mu = means[i]
+        assert abs(counts[:, i].mean() - mu) < 4 * math.sqrt(mu / 200)
+        assert abs(counts[:, i].var(ddof=1) / mu - 1) < 0.35
+
+
+def test_time_varying_constant_rate_matches_homogeneous_law():
+    """A single-piece rate function is a homogeneous Poisson process: same
+    mean and variance of counts as the gap-based generator (different draws)."""
+    a = W.Workload("h", [30.0], [W.fixed(1)], [W.fixed(1)], M=10, horizon_s=10.0, seed=5)
+    b = W.Workload("v", [30.0], [W.fixed(1)], [W.fixed(1)], M=10, horizon_s=10.0, seed=5)
+    b.rate_fn = [[(0.0, 30.0)]]
+    reps, mu = 300, 30.0 * 10.0
+    ca = [np.sum(oracle.gen_arrivals(a, r, 0, 800)[0] < 10 * TPS) for r in range(reps)]
+    cb = [np.sum(oracle.gen_arrivals(b, r, 0, 800)[0] < 10 * TPS) for r in range(reps)]
+    se = math.sqrt(mu / reps)  # standard error of a mean Poisson(mu) count
+    assert abs(np.mean(ca) - mu) < 4 * se and abs(np.mean(cb) - mu) < 4 * se
+    assert abs(np.var(cb, ddof=1) / mu - 1) < 0.3
+
+
+def test_time_varying_validation_reduces_to_constant_case():
+    """With constant pieces the time-varying check
+    reduces to the constant-rate conditions: Lambda^pi = dT * sum lambda and
+    p*_k = p_k (Eq. nested_wait_thresholds)."""
+    seg = [20, 40, 80, 160]
+    wl = W.Workload("c", list(W.C3A.lam), list(W.C3A.l_tab), list(W.C3A.lp_tab), M=W.C3A.M,
+                    horizon_s=10.0, seed=1)
+    wl.rate_fn = [[(0.0, lam)] for lam in W.C3A.lam]
+    n = [7, 7, 7, 5]
+    dT = fl.Fr(wl.d0_s) + fl.Fr(wl.d1_s) * fl.nested_memory_exact(wl, seg, n)
+    sup, pstar, ok = fl.validate_time_varying(wl, seg, n, dT)
+    assert sup == dT * sum(fl.Fr(x) for x in W.C3A.lam)
+    tails = fl.nested_tails(W.C3A, seg)
+    assert pstar[1:] == [tails[k] / tails[k - 1] for k in range(1, 4)]
+    assert ok == fl.nested_dT_ok(W.C3A, seg, n)
+    # the 1.5x peak of the day profile breaks the n_1 = 7 thresholds
+    tv = W.c3a_time_varying()
+    sup2, _, ok2 = fl.validate_time_varying(tv, seg, n, dT)
+    assert sup2 == dT * sum(fl.Fr(x) * fl.Fr(1.5) for x in W.C3A.lam) and not ok2

@@ -57,6 +57,9 @@ class Workload:
     d1_s: float = D1_S
     reps: int = 1               # replications the config is quoted on
     note: str = ""
+    # optional time-varying rates: per class a list of
+    # (start second, rate) pieces, first start 0; None / [] = constant lam
+    rate_fn: Optional[List[Optional[List[Tuple[float, float]]]]] = None
 
     @property
     def K(self) -> int:
@@ -191,3 +194,13 @@ def trace_arrays(arrivals: Sequence[Tuple[float, int, int, int]], tick_s: float 
         out.append((int(round(t / tick_s)), int(c), int(l), int(lp)))
     out.sort(key=lambda x: (x[0], x[1]))
     return out
+
+
+# Time-varying variant of C3a (NEXT(2)): the same four
+# types with a day-like profile -- rates scaled by 0.5x, 1.0x, 1.5x, 1.0x over
+# four 15-second periods (peak = 1.5x the C3a rates).
+def c3a_time_varying(profile=(0.5, 1.0, 1.5, 1.0), period_s: float = 15.0) -> Workload:
+    wl = Workload("C3a_tv", list(C3A.lam), list(C3A.l_tab), list(C3A.lp_tab), M=C3A.M,
+                  horizon_s=period_s * len(profile), seed=seed_for(9), reps=100_000)
+    wl.rate_fn = [[(i * period_s, lam * f) for i, f in enumerate(profile)] for lam in C3A.lam]
+    return wl
