@@ -1,14 +1,15 @@
-"""Benchmark of the hot path: batched WAIT / FCFS simulation of config C2.
+"""Benchmark of the hot path: the batched WAIT / Nested WAIT / FCFS simulation.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload C2|C1|C3a|C3b|C4|C5|C3a_tv] [--reps R]
 
-A step = one pass of the whole path over one batch of synthetic input:
-`sched_run` of R replications of config C2 (BASELINE.json configs[1]: two
-prompt types at the paper's low-demand lengths/rates, M = 7B KV budget)
-under WAIT (fluid-integer thresholds from `sched_thresholds`) AND under
-FCFS (B = 1024), then the per-policy aggregate and its single NCCL
-all-reduce.  Every step simulates fresh global replication indices.
-Weak scaling: every rank runs R replications per step.
+A step = one pass of the whole path over one batch of synthetic input: for
+every policy of the workload, one `sched_run` (C ABI) of R replications
+(fresh global replication indices every step), the per-policy aggregate,
+and the single NCCL all-reduce of the aggregates.  Weak scaling: every rank
+runs R replications per policy per step.  The default workload is C2
+(BASELINE.json configs[1]: two prompt types at the paper's low-demand
+lengths/rates, 7B KV budget, WAIT vs FCFS, 10^4 replications on 1 B200).
 Metric (BASELINE.json): simulated request-steps per second, whole job.
 """
 from __future__ import annotations
@@ -28,18 +29,69 @@ sys.path.insert(0, ROOT)
 METRIC = "simulated request-steps/sec (1/2/4/8 B200) + HBM GB/s vs peak; oracle ×speedup"
 UNIT = "request-steps/s"
 # algorithmic integer lane-ops per unit: request-step,
-# arrival (generated at visibility and again at admission), batch
+# arrival (Philox + -ln U + marks + scan share, generated at visibility and
+# regenerated at admission in the worst case), batch
 OPS_PER_REQUEST_STEP = 8
 OPS_PER_ARRIVAL = 400
 OPS_PER_BATCH = 100
 
 
-def workload_desc(wl, reps):
-    return {"workload": "C2: 2 prompt types (l,l',lambda)=(10,10,1000/s),(10,20,1000/s); "
-                        "M=131072 tokens; d0=12ms, d1=0.35us/token; T=10 s; WAIT fluid-integer "
-                        "thresholds + FCFS(vLLM new-first, B=1024)",
-            "replications_per_gpu_per_step": reps, "horizon_s": wl.horizon_s,
-            "policies": ["wait", "fcfs"]}
+def registry(name: str):
+    """(workload, [(label, Policy, thresholds or None = setup recipe)], reps, text)."""
+    import workloads as W
+    seg10 = [50 * k for k in range(1, 11)]
+    if name == "C2":
+        return (W.C2, [("wait", W.Policy(W.WAIT), None), ("fcfs", W.Policy(W.FCFS, B=1024), None)],
+                10_000, "C2: 2 prompt types (l,l',lambda)=(10,10,1000/s),(10,20,1000/s); M=131072 tokens; "
+                        "d0=12ms, d1=0.35us/token; T=10 s; WAIT fluid-integer thresholds + FCFS(vLLM "
+                        "new-first, B=1024)")
+    if name == "C1":
+        return (W.C1, [("wait", W.Policy(W.WAIT), None), ("fcfs", W.Policy(W.FCFS, B=32), None),
+                       ("nested", W.Policy(W.NESTED, seg_end=[16]), [1])],
+                16_384, "C1: 1 type (8,16,74/s), M=256, T=27.0 s; WAIT n=1, FCFS B=32, Nested 1 segment")
+    if name == "C3a":
+        return (W.C3A, [("nested", W.Policy(W.NESTED, seg_end=[20, 40, 80, 160]), None),
+                        ("fcfs", W.Policy(W.FCFS, B=1024), None)],
+                10_000, "C3a: 4 types l=10, l'=(20,40,80,160), rates 1:2:4:8 (rho=0.5), M=131072, "
+                        "T=60 s; Nested WAIT strict thresholds + FCFS B=1024")
+    if name == "C3a_tv":
+        return (W.c3a_time_varying(), [("nested", W.Policy(W.NESTED, seg_end=[20, 40, 80, 160]),
+                                        [11, 11, 10, 7]),
+                                       ("fcfs", W.Policy(W.FCFS, B=1024), None)],
+                10_000, "C3a with time-varying rates x(0.5,1,1.5,1) over 4x15 s (PAPER.md:1882); "
+                        "Nested WAIT (11,11,10,7) + FCFS B=1024")
+    if name == "C3b":
+        return (W.C3B, [("nested", W.Policy(W.NESTED, seg_end=seg10), None),
+                        ("fcfs", W.Policy(W.FCFS, B=2048), None)],
+                10_000, "C3b: geometric l' on [1,500], l=60, rho=0.3, M=524288, T=60 s; Nested L=10 + "
+                        "FCFS B=2048")
+    if name == "C4":
+        pols = []
+        for i in range(5):
+            pols += [(f"wait@{W.C4_RHO[i]}", W.Policy(W.WAIT), None, W.c4(i)),
+                     (f"nested@{W.C4_RHO[i]}", W.Policy(W.NESTED, seg_end=[100, 200, 300]), None, W.c4(i)),
+                     (f"fcfs@{W.C4_RHO[i]}", W.Policy(W.FCFS, B=1024), None, W.c4(i))]
+        return (None, pols, 2_000, "C4: heavy-traffic sweep, 3 types l=20, l'=(100,200,300), rates 3:2:1, "
+                                   "rho in {0.5,0.7,0.8,0.9,0.95} x {WAIT, Nested, FCFS}, T=20 s")
+    if name == "C5":
+        return (W.c5(55.0), [("nested", W.Policy(W.NESTED, seg_end=seg10), None),
+                             ("fcfs", W.Policy(W.FCFS, B=1024), None)],
+                2_048, "C5: chat-shaped marks (bins 23:11:8:7:6:4:3:2:1:1, prefill mean 60), 10^6 "
+                       "arrivals per trace (QPS 55, T=18182 s); Nested L=10 strict thresholds (M^pi > M: "
+                       "LIFO-eviction regime) + FCFS B=1024")
+    raise SystemExit(f"unknown workload {name}")
+
+
+# per-workload handle options (capacities sized for the long overloaded C5 traces)
+SCHED_KW = {"C5": dict(max_resident=4096, restart_cap=1 << 20)}
+
+
+def expand(name):
+    wl, pols, reps, text = registry(name)
+    out = []
+    for p in pols:
+        out.append(p if len(p) == 4 else (p[0], p[1], p[2], wl))
+    return out, reps, text
 
 
 class ClockSampler:
@@ -54,7 +106,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
@@ -91,17 +143,30 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(wl, policies, reps, threads, min_wall=1.5, max_reps=1 << 15):
+def oracle_thresholds(wl, pol, thr):
+    """Thresholds for the oracle legs: the given ones, else the oracle's own recipe."""
+    import workloads as W
+    from oracle import fluid as fl
+    if thr is not None:
+        return thr
+    if pol.kind == W.WAIT:
+        return fl.wait_fluid_integer(wl)
+    if pol.kind == W.NESTED:
+        return fl.nested_strict(wl, pol.seg_end)
+    return [0]
+
+
+def cpu_baseline(pols, reps, threads, min_wall=1.5, max_reps=1 << 15):
     """The oracle as it stands on the host cores, on a bounded sample: the
-    replication count doubles until one pass takes >= min_wall seconds
-    (>= 10-30 s of CPU work on a multi-core host).  Returns (rate, wall,
-    request_steps, reps)."""
+    replication count doubles until one pass takes >= min_wall seconds.
+    Returns (rate, wall, request_steps, reps per policy)."""
     import oracle
+    thr = [oracle_thresholds(wl, pol, t) for _, pol, t, wl in pols]
     while True:
         t0 = time.perf_counter()
         steps = 0
-        for pol, thr in policies:
-            rows = oracle.run(wl, pol, thr, n_reps=reps, rep_begin=0, n_threads=threads)
+        for (_, pol, _, wl), th in zip(pols, thr):
+            rows = oracle.run(wl, pol, th, n_reps=reps, rep_begin=0, n_threads=threads)
             steps += int(rows[oracle.F["request_steps"]].sum())
         dt = time.perf_counter() - t0
         if dt >= min_wall or reps >= max_reps:
@@ -111,35 +176,33 @@ def cpu_baseline(wl, policies, reps, threads, min_wall=1.5, max_reps=1 << 15):
 
 def run_reference(args):
     """--impl reference: the CPU oracle timed as the reference arm."""
-    rank, world, _ = (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), 0)
-    if rank != 0:
+    if int(os.environ.get("RANK", 0)) != 0:
         return
-    import workloads as W
-    from oracle import fluid as fl
-    wl = W.C2
-    pols = [(W.Policy(W.WAIT), fl.wait_fluid_integer(wl)), (W.Policy(W.FCFS, B=1024), [0])]
+    import oracle
+    pols, _, text = expand(args.workload)
+    thr = [oracle_thresholds(wl, pol, t) for _, pol, t, wl in pols]
     threads = os.cpu_count() or 1
     per_step = args.ref_reps
-    import oracle
     for _ in range(args.warmup):
-        oracle.run(wl, pols[0][0], pols[0][1], n_reps=min(per_step, threads), n_threads=threads)
+        _, pol, _, wl = pols[0]
+        oracle.run(wl, pol, thr[0], n_reps=min(per_step, threads), n_threads=threads)
     tot_steps, tot_t = 0, 0.0
     for k in range(args.steps):
         t0 = time.perf_counter()
-        for pol, thr in pols:
-            rows = oracle.run(wl, pol, thr, n_reps=per_step, rep_begin=k * per_step, n_threads=threads)
+        for (_, pol, _, wl), th in zip(pols, thr):
+            rows = oracle.run(wl, pol, th, n_reps=per_step, rep_begin=k * per_step, n_threads=threads)
             tot_steps += int(rows[oracle.F["request_steps"]].sum())
         tot_t += time.perf_counter() - t0
     v = tot_steps / tot_t
-    cfg = workload_desc(wl, per_step)
-    cfg["sample"] = f"{per_step} replications per policy per step (bounded sample of C2)"
+    sample = f"{per_step} replications per policy per step (bounded sample of {args.workload})"
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic (seeded Philox Poisson traces)", "config": cfg,
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
-                         "sample": cfg["sample"]},
+        "data": "synthetic (seeded Philox Poisson traces)",
+        "config": {"workload": text, "name": args.workload, "replications_per_policy_per_step": per_step,
+                   "sample": sample},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
@@ -150,9 +213,10 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--reps", type=int, default=10_000)
+    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--reps", type=int, default=0, help="replications per policy per GPU per step")
     ap.add_argument("--ref-reps", type=int, default=64)
-    ap.add_argument("--cpu-reps", type=int, default=256)
+    ap.add_argument("--cpu-reps", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -161,7 +225,7 @@ def main():
     import numpy as np
     import torch
 
-    import workloads as W
+    import paper_2504_11320_b200 as pkg
     from paper_2504_11320_b200 import Scheduler
     from paper_2504_11320_b200 import dist as D
     from paper_2504_11320_b200.sim import AGG_INT, aggregate, run_rows
@@ -169,21 +233,23 @@ def main():
     rank, world, local = D.init()
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
-    wl = W.C2
-    R = args.reps
-    s_wait = Scheduler(wl, W.Policy(W.WAIT), device=local)
-    thr_rep = s_wait.thresholds()           # product's own setup (sched_thresholds)
-    s_fcfs = Scheduler(wl, W.Policy(W.FCFS, B=1024), device=local)
-    scheds = [("wait", s_wait), ("fcfs", s_fcfs)]
-    rows = {n: torch.empty((len(__import__("paper_2504_11320_b200").FIELDS), R), dtype=torch.int64,
-                           device=dev) for n, _ in scheds}
+    pols, reps_default, text = expand(args.workload)
+    R = args.reps or reps_default
+    scheds, thr_used = [], {}
+    for label, pol, thr, wl in pols:
+        s = Scheduler(wl, pol, thr, device=local, **SCHED_KW.get(args.workload, {}))
+        if thr is None and pol.kind in (pkg.WAIT, pkg.NESTED):
+            thr_used[label] = s.thresholds()["thresholds"]  # product's own setup (sched_thresholds)
+        scheds.append((label, s, wl))
+    rows = {n: torch.empty((pkg.NF, R), dtype=torch.int64, device=dev) for n, _, _ in scheds}
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.int8, device=dev)  # > 126 MB L2
+    F_ = pkg.F
 
     def step(k, evs=None):
         begin, n = D.rep_range(k, rank, world, R)
         aggs = []
-        for i, (name, s) in enumerate(scheds):
+        for i, (name, s, wl) in enumerate(scheds):
             if evs is not None:
                 evs[i].record(stream)
             run_rows(s, wl.seed, begin, n, wl.horizon_s, rows[name], stream)
@@ -194,16 +260,15 @@ def main():
         return D.allreduce_aggregates(packed)  # S7: the one collective
 
     for k in range(args.warmup):
-        step(10_000 + k)
+        step(100_000 + k)
     torch.cuda.synchronize()
     D.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
-    t_step, t_kern = [], {n: [] for n, _ in scheds}
+    t_step, t_kern = [], {n: [] for n, _, _ in scheds}
     tot_int = None
-    units = {n: {"request_steps": 0, "arrivals": 0, "batches": 0, "completed": 0} for n, _ in scheds}
-    F_ = __import__("paper_2504_11320_b200").F
+    units = {n: {"request_steps": 0, "arrivals": 0, "batches": 0, "completed": 0} for n, _, _ in scheds}
     for k in range(args.steps):
         flush.zero_()
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(scheds) + 2)]
@@ -211,7 +276,7 @@ def main():
         evs[-1].record(stream)
         torch.cuda.synchronize()
         t_step.append(evs[0].elapsed_time(evs[-1]) / 1e3)
-        for i, (n, _) in enumerate(scheds):
+        for i, (n, _, _) in enumerate(scheds):
             t_kern[n].append(evs[i].elapsed_time(evs[i + 1]) / 1e3)
             r = rows[n]
             for u in units[n]:
@@ -223,24 +288,25 @@ def main():
     clk = clocks.stop()
     elapsed = D.max_over_ranks(sum(t_step), dev)
     nI = len(AGG_INT)
-    rs_idx = AGG_INT.index("request_steps")
-    total_rs = int(sum(tot_int[i * nI + rs_idx].item() for i in range(len(scheds))))
-    total_b = int(sum(tot_int[i * nI + AGG_INT.index("batches")].item() for i in range(len(scheds))))
-    total_c = int(sum(tot_int[i * nI + AGG_INT.index("completed")].item() for i in range(len(scheds))))
-    bad = int(sum(tot_int[i * nI + AGG_INT.index("status")].item() for i in range(len(scheds))))
+
+    def tot(field):
+        return int(sum(tot_int[i * nI + AGG_INT.index(field)].item() for i in range(len(scheds))))
+
+    bad = tot("status")
     if bad:
         raise SystemExit(f"{bad} replications reported a capacity status != 0: not a valid run")
-    value = total_rs / elapsed
+    value = tot("request_steps") / elapsed
 
     # e2e: the same metric through the host-buffer C-ABI call (D2H inside)
-    out_host = {n: np.zeros((len(F_), R), dtype=np.uint64) for n, _ in scheds}
+    out_host = {n: np.zeros((pkg.NF, R), dtype=np.uint64) for n, _, _ in scheds}
     torch.cuda.synchronize()
     D.barrier()
     t0 = time.perf_counter()
     e2e_rs = 0
-    for k in range(args.steps):
-        begin, n = D.rep_range(100 + k, rank, world, R)
-        for name, s in scheds:
+    e2e_steps = max(1, min(args.steps, 3))
+    for k in range(e2e_steps):
+        begin, n = D.rep_range(1000 + k, rank, world, R)
+        for name, s, wl in scheds:
             s.run_host(wl.seed, begin, n, wl.horizon_s, out_host[name], stream.cuda_stream)
             e2e_rs += int(out_host[name][F_["request_steps"]].sum())
     e2e_t = D.max_over_ranks(time.perf_counter() - t0, dev)
@@ -256,49 +322,47 @@ def main():
                       + OPS_PER_BATCH * u["batches"]) / args.steps
     dur = sum(t_kern[dom]) / len(t_kern[dom])
     props = torch.cuda.get_device_properties(dev)
+    sm_max, peak_src = 1965.0, "B200_PROFILING.md nominal clocks.max.sm (fallback)"
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    sm_max = 1965.0
     if os.path.exists(peaks_path):
-        sm_max = json.load(open(peaks_path)).get("sm_max_mhz", sm_max)
+        sm_max = float(json.load(open(peaks_path)).get("sm_max_mhz", sm_max))
+        peak_src = "MEASURED_PEAKS.json sm_max_mhz"
     peak_ops = props.multi_processor_count * 4 * 32 * sm_max * 1e6 / 1e12  # Tops/s
     achieved = ops_per_launch / dur / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(dom)
+        traffic = json.load(open(tp)).get(f"{args.workload}:{dom}")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic (seeded counter-based Philox Poisson traces, generated in-kernel)",
-        "config": dict(workload_desc(wl, R), parallelism=f"dp{world} (replication sharding)",
-                       l2="256 MiB buffer written between timed steps (L2 flush)",
-                       wait_thresholds=thr_rep["thresholds"]),
-        "batch_steps_per_s": total_b / elapsed, "requests_per_s": total_c / elapsed,
-        "status_errors": bad,
+        "config": {"workload": text, "name": args.workload, "replications_per_policy_per_gpu_per_step": R,
+                   "policies": [n for n, _, _ in scheds], "parallelism": f"dp{world} (replication sharding)",
+                   "l2": "256 MiB buffer written between timed steps (L2 flush)",
+                   "thresholds_from_sched_thresholds": thr_used},
+        "batch_steps_per_s": tot("batches") / elapsed, "requests_per_s": tot("completed") / elapsed,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": len(F_) * R * 8 * len(scheds),
-                "note": "sched_run_host: launch + D2H of the metric rows + sync; inputs are seeds "
-                        "(kernel arguments) so no H2D input bytes"},
-        "gpu_launches": len(scheds) * args.steps,
+                "d2h_bytes_per_step": pkg.NF * R * 8 * len(scheds),
+                "note": "sched_run_host: launch + D2H of the metric rows + sync; the step's inputs are "
+                        "seeds and replication indices (kernel arguments), so no H2D input bytes"},
+        "gpu_launches": sum(1 + (1 if s.launch_info()["fallback_grid"] else 0) for _, s, _ in scheds)
+        * args.steps,
         "roofline": {"bound": "alu", "kernel": f"sim_kernel<{dom}>", "achieved": achieved,
-                     "peak": peak_ops, "unit": "Tops/s", "frac": achieved / peak_ops,
-                     "traffic": traffic,
+                     "peak": peak_ops, "unit": "Tops/s", "frac": achieved / peak_ops, "traffic": traffic,
                      "ops_model": f"{OPS_PER_REQUEST_STEP}/request-step + {OPS_PER_ARRIVAL}/arrival "
-                                  f"+ {OPS_PER_BATCH}/batch (integer lane-ops)",
+                                  f"+ {OPS_PER_BATCH}/batch (integer lane-ops, DESIGN.md §5.4)",
                      "peak_basis": f"{props.multi_processor_count} SMs x 4 warp-instr/clk x 32 lanes x "
-                                   f"{sm_max:.0f} MHz (MEASURED_PEAKS sm_max)"},
+                                   f"{sm_max:.0f} MHz ({peak_src})"},
         "kernel_ms": {n: 1e3 * sum(v) / len(v) for n, v in t_kern.items()},
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        import workloads as W2
-        from oracle import fluid as fl
         threads = os.cpu_count() or 1
-        pols = [(W2.Policy(W2.WAIT), fl.wait_fluid_integer(wl)), (W2.Policy(W2.FCFS, B=1024), [0])]
-        v, dt, n, nr = cpu_baseline(wl, pols, args.cpu_reps, threads)
+        v, dt, n, nr = cpu_baseline(pols, args.cpu_reps, threads)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
-                                "sample": f"C2 full horizon, {nr} replications x 2 policies "
+                                "sample": f"{args.workload}, {nr} replications per policy "
                                           f"({n} request-steps, {dt:.2f} s wall on {threads} threads)"}
     if rank == 0:
         print(json.dumps(line))
