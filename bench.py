@@ -310,10 +310,7 @@ def main():
             s.run_host(wl.seed, begin, n, wl.horizon_s, out_host[name], stream.cuda_stream)
             e2e_rs += int(out_host[name][F_["request_steps"]].sum())
     e2e_t = D.max_over_ranks(time.perf_counter() - t0, dev)
-    e2e_tot = torch.tensor([float(e2e_rs)], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(e2e_tot)
-    e2e_value = float(e2e_tot.item()) / e2e_t
+    e2e_value = D.sum_over_ranks(float(e2e_rs), dev) / e2e_t
 
     # roofline of the dominant kernel (alu/issue bound)
     dom = max(t_kern, key=lambda n: sum(t_kern[n]))

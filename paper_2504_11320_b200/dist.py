@@ -21,7 +21,14 @@ def env_rank() -> Tuple[int, int, int]:
 
 
 def init(backend: str = None) -> Tuple[int, int, int]:
+    """Process group for the single metric all-reduce: NCCL (one process
+    per GPU) by default; WAITSIM_DIST_BACKEND=gloo runs the same code with a
+    host-side reduce (used to exercise N>1 on fewer GPUs).  Returns (rank,
+    world, device index)."""
     rank, world, local = env_rank()
+    backend = backend or os.environ.get("WAITSIM_DIST_BACKEND")
+    if torch.cuda.is_available():
+        local = local % torch.cuda.device_count()
     if world > 1 and not dist.is_initialized():
         if backend is None:
             backend = "nccl" if torch.cuda.is_available() else "gloo"
@@ -32,6 +39,20 @@ def init(backend: str = None) -> Tuple[int, int, int]:
         else:
             dist.init_process_group(backend)
     return rank, world, local
+
+
+def _host_reduce() -> bool:
+    return dist.get_backend() == "gloo"
+
+
+def _all_reduce(t: torch.Tensor, op=None) -> torch.Tensor:
+    op = op if op is not None else dist.ReduceOp.SUM
+    if t.is_cuda and _host_reduce():
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        return h.to(t.device)
+    dist.all_reduce(t, op=op)
+    return t
 
 
 def rep_range(step: int, rank: int, world: int, per_rank: int) -> Tuple[int, int]:
@@ -54,8 +75,7 @@ def allreduce_aggregates(agg: Dict[str, torch.Tensor]) -> Dict[str, torch.Tensor
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return agg
     ints, f64 = agg["int"], agg["f64"]
-    buf = torch.cat([ints.to(torch.float64), f64])
-    dist.all_reduce(buf)
+    buf = _all_reduce(torch.cat([ints.to(torch.float64), f64]))
     n = ints.numel()
     return {"int": buf[:n].round().to(torch.int64), "f64": buf[n:]}
 
@@ -64,8 +84,14 @@ def max_over_ranks(x: float, device=None) -> float:
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return x
     t = torch.tensor([x], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return float(_all_reduce(t, dist.ReduceOp.MAX).item())
+
+
+def sum_over_ranks(x: float, device=None) -> float:
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    return float(_all_reduce(t).item())
 
 
 def barrier():
