@@ -425,14 +425,16 @@ int sched_create(sched_t* out, const sched_config* cfg) {
   h->h_cdf_thr = std::move(thr_all);
   h->h_cdf_val = std::move(val_all);
   if (cfg->policy == SCHED_NESTED) {
-    // stage -> segment index | entry-stage flag << 7 (reading R8)
+    // stage -> segment index (bits 0-5, 63 = beyond the last segment) |
+    // last stage of its segment << 6 | entry stage << 7 (reading R8)
     std::vector<uint8_t> info(in.seg_end.back() + 2, 0);
     for (uint32_t s = 0; s < info.size(); ++s) {
       uint32_t k = 0;
       while (k < in.seg_end.size() && s > in.seg_end[k]) ++k;
-      if (k >= in.seg_end.size()) k = 0x7F;
-      const bool entry = k >= 1 && k < in.seg_end.size() && s == (uint32_t)in.seg_end[k - 1] + 1;
-      info[s] = (uint8_t)(k | (entry ? 0x80 : 0));
+      const bool valid = k < in.seg_end.size();
+      const bool entry = valid && k >= 1 && s == (uint32_t)in.seg_end[k - 1] + 1;
+      const bool last = valid && s == (uint32_t)in.seg_end[k];
+      info[s] = (uint8_t)((valid ? k : 0x3F) | (last ? 0x40 : 0) | (entry ? 0x80 : 0));
     }
     h->h_stage_info = std::move(info);
   }

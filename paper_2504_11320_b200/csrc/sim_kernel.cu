@@ -233,9 +233,11 @@ struct WarpSim {
   __device__ __forceinline__ size_t ring_slot(int q, uint32_t pos) const {
     return ring_base + (size_t)q * P.ring_cap + (pos % P.ring_cap);
   }
-  __device__ __forceinline__ uint32_t nested_key(uint32_t s) const {  // counter slot of stage s
-    const uint32_t info = __ldg(P.stage_info + s);
-    return (info & 0x7F) + ((info >> 7) ? 32u : 0u);
+  // NESTED stage info: segment index (bits 0-5), last stage of the segment
+  // (bit 6), entry stage (bit 7); counter slot = segment (+32 at entry)
+  __device__ __forceinline__ static uint32_t info_seg(uint32_t info) { return info & 0x3F; }
+  __device__ __forceinline__ static uint32_t info_key(uint32_t info) {
+    return (info & 0x3F) + ((info >> 7) ? 32u : 0u);
   }
 
   // ---------------------------------------------------- S1 arrival windows
@@ -642,8 +644,8 @@ struct WarpSim {
       if (POL == SCHED_WAIT) inp = valid && ((Qmask >> (meta & 0xFF)) & 1u);
       if (POL == SCHED_NESTED) {
         const uint32_t info = valid ? __ldg(P.stage_info + s) : 0u;
-        const int seg = info & 0x7F;
-        nkey = (info & 0x7F) + ((info >> 7) ? 32u : 0u);
+        const int seg = info_seg(info);
+        nkey = info_key(info);
         const bool entry = valid && (info >> 7) && seg <= kstar;
         const uint32_t key = entry ? s : (0x10000u + lane);
         const uint32_t grp = __match_any_sync(FULL, key);
@@ -727,7 +729,12 @@ struct WarpSim {
   // per-member update, completions, compaction; counters updated in place.
   __device__ void execute(uint32_t n_evict, int64_t peak, uint32_t waiting) {
     const uint32_t n_tot = n_res + n_new;
-    if (POL == SCHED_NESTED) { rank[lane] = 0; __syncwarp(); }
+    uint32_t over = 0;  // NESTED: active segments whose entry queue exceeds n_k
+    if (POL == SCHED_NESTED) {
+      over = __ballot_sync(FULL, lane >= 1 && lane <= kstar && cnt[32 + lane] > P.thr[lane]);
+      rank[lane] = 0;
+      __syncwarp();
+    }
     uint32_t tok = 0, n_done = 0, done_tok = 0, n_ft = 0, kv_free = 0, grow = 0;
     uint64_t done_a = 0, ft_a = 0;
     uint32_t wp = 0;
@@ -742,18 +749,23 @@ struct WarpSim {
       const uint32_t s = (uint32_t)((qv >> 32) & 0xFFFF);
       uint32_t meta = (uint32_t)(qv >> 48);
       bool inp = false;
-      uint32_t key_s = 0;
+      uint32_t key_s = 0, info_s = 0;
       if (POL == SCHED_NESTED) {
-        const uint32_t info = (valid && !fresh) ? __ldg(P.stage_info + s) : 0x7Fu;
-        const int seg = info & 0x7F;
-        key_s = (info & 0x7F) + ((info >> 7) ? 32u : 0u);
+        info_s = (valid && !fresh) ? __ldg(P.stage_info + s) : 0x3Fu;
+        const int seg = info_seg(info_s);
+        key_s = info_key(info_s);
         const bool act = valid && !fresh && seg <= kstar;
-        const bool entry = act && (info >> 7);
-        const uint32_t key = entry ? s : (0x10000u + lane);
-        const uint32_t grp = __match_any_sync(FULL, key);
-        if (act) inp = entry ? (rank[seg] + __popc(grp & lanemask_lt()) < P.thr[seg]) : true;
-        __syncwarp();
-        if (entry && (grp & lanemask_lt()) == 0) rank[seg] += __popc(grp);
+        // entry-stage residents need a rank only in segments whose entry
+        // queue holds more than n_k (first n_k in admission order batch)
+        const bool ranked = act && (info_s >> 7) && ((over >> seg) & 1u);
+        inp = act;
+        if (__any_sync(FULL, ranked)) {
+          const uint32_t key = ranked ? s : (0x10000u + lane);
+          const uint32_t grp = __match_any_sync(FULL, key);
+          if (ranked) inp = rank[seg] + __popc(grp & lanemask_lt()) < P.thr[seg];
+          __syncwarp();
+          if (ranked && (grp & lanemask_lt()) == 0) rank[seg] += __popc(grp);
+        }
       } else if (POL == SCHED_WAIT) {
         inp = valid && !fresh && ((Qmask >> (meta & 0xFF)) & 1u);
       } else {
@@ -777,9 +789,13 @@ struct WarpSim {
         } else {
           ns = s + 1;
           ++grow;
-          if (POL == SCHED_NESTED) {
-            const uint32_t key_n = nested_key(ns);
-            if (key_n != key_s) { atomicSub(&cnt[key_s], 1u); atomicAdd(&cnt[key_n], 1u); }
+          if (POL == SCHED_NESTED && (info_s & 0xC0)) {
+            // leaving an entry stage (-> non-entry) or a segment's last stage
+            // (-> the next segment's entry stage)
+            const uint32_t seg = info_seg(info_s);
+            const uint32_t key_n = (info_s & 0x40) ? 32u + seg + 1u : seg;
+            atomicSub(&cnt[key_s], 1u);
+            atomicAdd(&cnt[key_n], 1u);
           }
         }
       }
