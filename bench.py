@@ -246,16 +246,22 @@ def main():
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.int8, device=dev)  # > 126 MB L2
     F_ = pkg.F
 
-    def step(k, evs=None):
+    # every policy's launch on its own stream, so independent launches share
+    # the GPU (a C4 sweep point alone does not fill 148 SMs)
+    pstreams = [torch.cuda.Stream(dev) for _ in scheds]
+
+    def step(k, ev_start=None, ev_ends=None):
         begin, n = D.rep_range(k, rank, world, R)
-        aggs = []
+        start = ev_start or torch.cuda.Event()
+        start.record(stream)
+        ends = ev_ends or [torch.cuda.Event() for _ in scheds]
         for i, (name, s, wl) in enumerate(scheds):
-            if evs is not None:
-                evs[i].record(stream)
-            run_rows(s, wl.seed, begin, n, wl.horizon_s, rows[name], stream)
-            aggs.append(aggregate(rows[name], wl.horizon_s))
-        if evs is not None:
-            evs[len(scheds)].record(stream)
+            pstreams[i].wait_event(start)
+            run_rows(s, wl.seed, begin, n, wl.horizon_s, rows[name], pstreams[i])
+            ends[i].record(pstreams[i])
+        for e in ends:
+            stream.wait_event(e)
+        aggs = [aggregate(rows[name], wl.horizon_s) for name, _, wl in scheds]
         packed = {"int": torch.cat([a["int"] for a in aggs]), "f64": torch.cat([a["f64"] for a in aggs])}
         return D.allreduce_aggregates(packed)  # S7: the one collective
 
@@ -271,13 +277,15 @@ def main():
     units = {n: {"request_steps": 0, "arrivals": 0, "batches": 0, "completed": 0} for n, _, _ in scheds}
     for k in range(args.steps):
         flush.zero_()
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(scheds) + 2)]
-        agg = step(k, evs[:len(scheds) + 1])
-        evs[-1].record(stream)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ends = [torch.cuda.Event(enable_timing=True) for _ in scheds]
+        ev1 = torch.cuda.Event(enable_timing=True)
+        agg = step(k, ev0, ends)
+        ev1.record(stream)
         torch.cuda.synchronize()
-        t_step.append(evs[0].elapsed_time(evs[-1]) / 1e3)
+        t_step.append(ev0.elapsed_time(ev1) / 1e3)
         for i, (n, _, _) in enumerate(scheds):
-            t_kern[n].append(evs[i].elapsed_time(evs[i + 1]) / 1e3)
+            t_kern[n].append(ev0.elapsed_time(ends[i]) / 1e3)  # concurrent: start -> its end
             r = rows[n]
             for u in units[n]:
                 units[n][u] += int(r[F_[u]].sum().item())
@@ -312,12 +320,24 @@ def main():
     e2e_t = D.max_over_ranks(time.perf_counter() - t0, dev)
     e2e_value = D.sum_over_ranks(float(e2e_rs), dev) / e2e_t
 
-    # roofline of the dominant kernel (alu/issue bound)
-    dom = max(t_kern, key=lambda n: sum(t_kern[n]))
-    u = units[dom]
+    # roofline of the dominant kernel (alu/issue bound),
+    # timed alone (no concurrent launches) on its own stream
+    dom = max(units, key=lambda n: units[n]["request_steps"])
+    di = [n for n, _, _ in scheds].index(dom)
+    _, s_dom, wl_dom = scheds[di]
+    solo = []
+    for k in range(3):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        begin, n = D.rep_range(2000 + k, rank, world, R)
+        a.record(pstreams[di])
+        run_rows(s_dom, wl_dom.seed, begin, n, wl_dom.horizon_s, rows[dom], pstreams[di])
+        b.record(pstreams[di])
+        torch.cuda.synchronize()
+        solo.append((a.elapsed_time(b) / 1e3, {u: int(rows[dom][F_[u]].sum().item()) for u in units[dom]}))
+    dur, u = solo[-1]
     ops_per_launch = (OPS_PER_REQUEST_STEP * u["request_steps"] + OPS_PER_ARRIVAL * u["arrivals"]
-                      + OPS_PER_BATCH * u["batches"]) / args.steps
-    dur = sum(t_kern[dom]) / len(t_kern[dom])
+                      + OPS_PER_BATCH * u["batches"])
     props = torch.cuda.get_device_properties(dev)
     sm_max, peak_src = 1965.0, "B200_PROFILING.md nominal clocks.max.sm (fallback)"
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -353,6 +373,9 @@ def main():
                      "peak_basis": f"{props.multi_processor_count} SMs x 4 warp-instr/clk x 32 lanes x "
                                    f"{sm_max:.0f} MHz ({peak_src})"},
         "kernel_ms": {n: 1e3 * sum(v) / len(v) for n, v in t_kern.items()},
+        "kernel_ms_note": "per policy: step start -> that launch's end (launches run concurrently on "
+                          "separate streams); roofline uses the dominant launch timed alone",
+        "dominant_alone_ms": 1e3 * dur,
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
