@@ -724,6 +724,94 @@ struct WarpSim {
     peak = P.M + excess;
   }
 
+  // per-lane batch accumulators of the execute pass
+  struct Acc {
+    uint32_t tok = 0, n_done = 0, done_tok = 0, n_ft = 0, kv_free = 0, grow = 0;
+    uint64_t done_a = 0, ft_a = 0;
+  };
+  struct Upd {
+    bool keep, inp;
+    uint32_t l, lp, ns, meta;
+  };
+
+  // S5 per-member step: membership, first token, completion or s++
+  __device__ __forceinline__ Upd member(bool valid, bool fresh, int64_t a, uint64_t qv,
+                                        uint32_t over, Acc& acc) {
+    Upd u;
+    u.l = (uint32_t)(qv & 0xFFFF);
+    u.lp = (uint32_t)((qv >> 16) & 0xFFFF);
+    const uint32_t s = (uint32_t)((qv >> 32) & 0xFFFF);
+    u.meta = (uint32_t)(qv >> 48);
+    bool inp = false;
+    uint32_t key_s = 0, info_s = 0;
+    if (POL == SCHED_NESTED) {
+      info_s = (valid && !fresh) ? __ldg(P.stage_info + s) : 0x3Fu;
+      const int seg = info_seg(info_s);
+      key_s = info_key(info_s);
+      const bool act = valid && !fresh && seg <= kstar;
+      // entry-stage residents need a rank only in segments whose entry
+      // queue holds more than n_k (first n_k in admission order batch)
+      const bool ranked = act && (info_s >> 7) && ((over >> seg) & 1u);
+      inp = act;
+      if (__any_sync(FULL, ranked)) {
+        const uint32_t key = ranked ? s : (0x10000u + lane);
+        const uint32_t grp = __match_any_sync(FULL, key);
+        if (ranked) inp = rank[seg] + __popc(grp & lanemask_lt()) < P.thr[seg];
+        __syncwarp();
+        if (ranked && (grp & lanemask_lt()) == 0) rank[seg] += __popc(grp);
+        __syncwarp();
+      }
+    } else if (POL == SCHED_WAIT) {
+      inp = valid && !fresh && ((Qmask >> (u.meta & 0xFF)) & 1u);
+    } else {
+      inp = valid && !fresh;
+    }
+    u.keep = valid;
+    u.inp = inp;
+    u.ns = s;
+    if (inp) {
+      acc.tok += u.l + s;
+      // the stage-1 iteration emits the first output token
+      if (s == 1 && !(u.meta & META_FT)) { u.meta |= META_FT; ++acc.n_ft; acc.ft_a += (uint64_t)a; }
+      if (s == u.lp) {
+        // stage l' done: complete, free KV
+        u.keep = false;
+        acc.kv_free += u.l + u.lp - 1;
+        ++acc.n_done;
+        acc.done_tok += u.lp;
+        acc.done_a += (uint64_t)a;
+        if (POL == SCHED_WAIT) atomicSub(&cnt[u.meta & 0xFF], 1u);
+        if (POL == SCHED_NESTED) atomicSub(&cnt[key_s], 1u);
+      } else {
+        u.ns = s + 1;
+        ++acc.grow;
+        if (POL == SCHED_NESTED && (info_s & 0xC0)) {
+          // leaving an entry stage (-> non-entry) or a segment's last stage
+          // (-> the next segment's entry stage)
+          const uint32_t seg = info_seg(info_s);
+          const uint32_t key_n = (info_s & 0x40) ? 32u + seg + 1u : seg;
+          atomicSub(&cnt[key_s], 1u);
+          atomicAdd(&cnt[key_n], 1u);
+        }
+      }
+    }
+    return u;
+  }
+
+  // in-place stream compaction of one chunk (ballot + popc keeps order)
+  __device__ __forceinline__ void compact(const Upd& u, uint32_t i, int64_t a, uint64_t qv,
+                                          uint32_t& wp) {
+    const uint32_t km = __ballot_sync(FULL, u.keep);
+    const uint32_t d = wp + __popc(km & lanemask_lt());
+    __syncwarp();
+    if (u.keep) {
+      if (d != i) { ra[d] = a; rq[d] = pack_q(u.l, u.lp, u.ns, u.meta); }
+      else if (u.inp) rq[d] = pack_q(u.l, u.lp, u.ns, u.meta);
+    }
+    wp += __popc(km);
+    __syncwarp();
+  }
+
   // ------------------------------------------------------ S5 execute
   // One pass over residents (+ the staged admissions) in admission order:
   // per-member update, completions, compaction; counters updated in place.
@@ -735,80 +823,38 @@ struct WarpSim {
       rank[lane] = 0;
       __syncwarp();
     }
-    uint32_t tok = 0, n_done = 0, done_tok = 0, n_ft = 0, kv_free = 0, grow = 0;
-    uint64_t done_a = 0, ft_a = 0;
+    Acc acc;
     uint32_t wp = 0;
-    for (uint32_t base = 0; base < n_tot; base += 32) {
-      const uint32_t i = base + lane;
-      const bool valid = i < n_tot;
-      const bool fresh = i >= n_res;
-      int64_t a = 0;
-      uint64_t qv = 0;
-      if (valid) { a = ra[i]; qv = rq[i]; }
-      const uint32_t l = (uint32_t)(qv & 0xFFFF), lp = (uint32_t)((qv >> 16) & 0xFFFF);
-      const uint32_t s = (uint32_t)((qv >> 32) & 0xFFFF);
-      uint32_t meta = (uint32_t)(qv >> 48);
-      bool inp = false;
-      uint32_t key_s = 0, info_s = 0;
-      if (POL == SCHED_NESTED) {
-        info_s = (valid && !fresh) ? __ldg(P.stage_info + s) : 0x3Fu;
-        const int seg = info_seg(info_s);
-        key_s = info_key(info_s);
-        const bool act = valid && !fresh && seg <= kstar;
-        // entry-stage residents need a rank only in segments whose entry
-        // queue holds more than n_k (first n_k in admission order batch)
-        const bool ranked = act && (info_s >> 7) && ((over >> seg) & 1u);
-        inp = act;
-        if (__any_sync(FULL, ranked)) {
-          const uint32_t key = ranked ? s : (0x10000u + lane);
-          const uint32_t grp = __match_any_sync(FULL, key);
-          if (ranked) inp = rank[seg] + __popc(grp & lanemask_lt()) < P.thr[seg];
-          __syncwarp();
-          if (ranked && (grp & lanemask_lt()) == 0) rank[seg] += __popc(grp);
-        }
-      } else if (POL == SCHED_WAIT) {
-        inp = valid && !fresh && ((Qmask >> (meta & 0xFF)) & 1u);
-      } else {
-        inp = valid && !fresh;
+    // two chunks per iteration: both chunks' loads issue before the first
+    // chunk's dependent chain (ILP); compaction stays in admission order
+    // (chunk 0's writes land below chunk 1's read positions)
+    if (POL == SCHED_WAIT) {  // register-bound at 20 warps/SM: one chunk at a time
+      for (uint32_t base = 0; base < n_tot; base += 32) {
+        const uint32_t i0 = base + lane;
+        const bool v0 = i0 < n_tot;
+        int64_t a0 = 0;
+        uint64_t q0 = 0;
+        if (v0) { a0 = ra[i0]; q0 = rq[i0]; }
+        const Upd u0 = member(v0, i0 >= n_res, a0, q0, over, acc);
+        compact(u0, i0, a0, q0, wp);
       }
-      bool keep = valid;
-      uint32_t ns = s;
-      if (inp) {
-        tok += l + s;
-        // the stage-1 iteration emits the first output token
-        if (s == 1 && !(meta & META_FT)) { meta |= META_FT; ++n_ft; ft_a += (uint64_t)a; }
-        if (s == lp) {
-          // stage l' done: complete, free KV
-          keep = false;
-          kv_free += l + lp - 1;
-          ++n_done;
-          done_tok += lp;
-          done_a += (uint64_t)a;
-          if (POL == SCHED_WAIT) atomicSub(&cnt[meta & 0xFF], 1u);
-          if (POL == SCHED_NESTED) atomicSub(&cnt[key_s], 1u);
-        } else {
-          ns = s + 1;
-          ++grow;
-          if (POL == SCHED_NESTED && (info_s & 0xC0)) {
-            // leaving an entry stage (-> non-entry) or a segment's last stage
-            // (-> the next segment's entry stage)
-            const uint32_t seg = info_seg(info_s);
-            const uint32_t key_n = (info_s & 0x40) ? 32u + seg + 1u : seg;
-            atomicSub(&cnt[key_s], 1u);
-            atomicAdd(&cnt[key_n], 1u);
-          }
-        }
+    } else {
+      for (uint32_t base = 0; base < n_tot; base += 64) {
+        const uint32_t i0 = base + lane, i1 = i0 + 32;
+        const bool v0 = i0 < n_tot, v1 = i1 < n_tot;
+        int64_t a0 = 0, a1 = 0;
+        uint64_t q0 = 0, q1 = 0;
+        if (v0) { a0 = ra[i0]; q0 = rq[i0]; }
+        if (v1) { a1 = ra[i1]; q1 = rq[i1]; }
+        const Upd u0 = member(v0, i0 >= n_res, a0, q0, over, acc);
+        const Upd u1 = member(v1, i1 >= n_res, a1, q1, over, acc);
+        compact(u0, i0, a0, q0, wp);
+        compact(u1, i1, a1, q1, wp);
       }
-      const uint32_t km = __ballot_sync(FULL, keep);
-      const uint32_t d = wp + __popc(km & lanemask_lt());
-      __syncwarp();
-      if (keep) {
-        if (d != i) { ra[d] = a; rq[d] = pack_q(l, lp, ns, meta); }
-        else if (inp) rq[d] = pack_q(l, lp, ns, meta);
-      }
-      wp += __popc(km);
-      __syncwarp();
     }
+    uint32_t tok = acc.tok, n_done = acc.n_done, done_tok = acc.done_tok, n_ft = acc.n_ft,
+             kv_free = acc.kv_free, grow = acc.grow;
+    const uint64_t done_a = acc.done_a, ft_a = acc.ft_a;
     if (POL == SCHED_WAIT) { if (lane < P.K) cnt[lane] += newc; }
     if (POL == SCHED_NESTED) { if (lane == 0) cnt[0] += n_new; }  // stage 1 = segment 1, non-entry
     // warp-uniform batch totals
@@ -957,7 +1003,10 @@ struct WarpSim {
 };
 
 template <int POL, bool TRACE>
-__global__ void __launch_bounds__(256, POL == SCHED_WAIT ? 3 : 2) sim_kernel(const DevParams P) {
+// WAIT: <= 4 warps per block, 5 blocks per SM -> <= 102 registers (20 warps/SM
+// at C2's shared-memory footprint); others are shared-memory bound: 128 regs
+__global__ void __launch_bounds__(POL == SCHED_WAIT ? 128 : 256, POL == SCHED_WAIT ? 5 : 2)
+    sim_kernel(const DevParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;

@@ -1,4 +1,5 @@
-for i in 1 2; do
-LIB=paper_2504_11320_b200/libsched_prev.so WL=C2 python tools/time_run.py
-WL=C2 python tools/time_run.py
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -3 gpurun_out/pytest_gpu.log
+for wl in C2 C3a C4_2; do
+LIB=paper_2504_11320_b200/libsched_prev.so WL=$wl python tools/time_run.py | sed 's/^/prev /'
+WL=$wl python tools/time_run.py | sed 's/^/new  /'
 done
