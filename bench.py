@@ -207,6 +207,75 @@ def run_reference(args):
     }))
 
 
+def bench_walks(args):
+    """--workload walks: the appendix random-walk chains (NEXT(4)) through
+    sched_walks; metric = simulated walk-steps per second (weak scaling)."""
+    import torch
+    from paper_2504_11320_b200 import dist as D
+    from paper_2504_11320_b200._lib import WALK_FIELDS, walks, walks_device
+    rank, world, local = D.init()
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    N = args.reps or (1 << 20)
+    B = 1000
+    cases = [dict(kind=0, n=8, mu=8.0), dict(kind=1, n=6, n_prev=10, p=0.5)]
+    out = torch.empty((len(WALK_FIELDS), N), dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(k):
+        for j, c in enumerate(cases):
+            walks_device(c["kind"], c["n"], B, N, seed=0x2504113200000011,
+                         out_ptr=out.data_ptr(), walk_begin=(k * world + rank) * N,
+                         mu=c.get("mu", 0.0), n_prev=c.get("n_prev", 0), p=c.get("p", 0.0),
+                         stream_ptr=stream.cuda_stream)
+
+    for k in range(args.warmup):
+        step(1000 + k)
+    torch.cuda.synchronize()
+    D.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for k in range(args.steps):
+        step(k)
+    b.record(stream)
+    torch.cuda.synchronize()
+    D.barrier()
+    clk = clocks.stop()
+    el = D.max_over_ranks(a.elapsed_time(b) / 1e3, dev)
+    steps_total = world * args.steps * len(cases) * N * B
+    value = steps_total / el
+    # per walk-step: Philox 10 rounds (~100 lane-ops) + pmf inversion (~4 ops
+    # per unit of the mean arrivals + 8) + the chain and coupled updates (~20)
+    ops = sum(100 + 8 + 4 * (c.get("mu") or c["n_prev"] * c["p"]) + 20 for c in cases) / len(cases)
+    props = torch.cuda.get_device_properties(dev)
+    sm_max = 1965.0
+    pp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pp):
+        sm_max = float(json.load(open(pp)).get("sm_max_mhz", sm_max))
+    peak = props.multi_processor_count * 128 * sm_max * 1e6 / 1e12
+    ach = value * ops / 1e12
+    t0 = time.perf_counter()
+    walks(0, 8, B, min(N, 65536), seed=1, mu=8.0, device=local)
+    e2e = min(N, 65536) * B / (time.perf_counter() - t0)
+    line = {"metric": "simulated walk-steps/sec (appendix random-walk chains, NEXT(4))",
+            "value": value, "unit": "walk-steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
+            "data": "synthetic (Philox draws)", "config": {"workload": "walks", "walks_per_case": N,
+                                                          "steps_per_walk": B, "cases": cases},
+            "e2e": {"value": e2e, "unit": "walk-steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": len(WALK_FIELDS) * 8 * min(N, 65536)},
+            "gpu_launches": len(cases) * args.steps,
+            "roofline": {"bound": "alu", "kernel": "walk_kernel", "achieved": ach, "peak": peak,
+                         "unit": "Tops/s", "frac": ach / peak, "traffic": None,
+                         "ops_model": f"{ops:.0f} lane-ops per walk-step"},
+            "clocks": clk}
+    if rank == 0:
+        print(json.dumps(line))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -221,6 +290,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "walks":
+        return bench_walks(args)
 
     import numpy as np
     import torch

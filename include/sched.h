@@ -194,6 +194,30 @@ typedef struct {
 } sched_launch_info;
 int sched_get_launch_info(sched_t h, sched_launch_info* out);
 
+/* NEXT(4): the appendix's embedded random-walk chains, one thread per walk
+ * (App. B-C).  kind 0: the WAIT chain of Lemma
+ * "Queue Length and Stuck Time" with X^b ~ Poisson(mu) and
+ * threshold n, plus its coupled dominating process started at 2n (Lemma,
+ * PAPER.md:2169).  kind 1: the Nested segment-k chain with binomial thinning
+ * Y^b ~ Binomial(n_prev, p) and threshold n, coupled process started at n
+ * (PAPER.md:2290-2310).  B steps per walk; walks walk_begin ..
+ * walk_begin+n_walks-1 (global indices: sharding-invariant).  Output:
+ * field-major int64 [SCHED_WALK_NF][n_walks]: W^B, stuck iterations,
+ * sum_b W^b, max_b W^b, coupled W~^B, dominance violations (#b with
+ * W~^b < W^b + n (kind 0) or < W^b (kind 1); 0 by the Lemmas), sum of
+ * arrivals, max_{i<=B} S^i, min_{i<=B} S^i, S^B (S^i = partial sums of
+ * arrivals - n).  sched_walks: device output, async on `cuda_stream`;
+ * sched_walks_host: host output, synchronous on `device`.
+ * Errors: SCHED_E_INVALID (kind, n < 1, mu <= 0 or > 1e4, n_prev < 1,
+ * p outside (0,1), n_walks = 0, B = 0, walk index >= 2^32), SCHED_E_CUDA. */
+enum { SCHED_WALK_NF = 10 };
+int sched_walks(int32_t kind, int64_t n, double mu, int64_t n_prev, double p, uint64_t seed,
+                uint64_t walk_begin, uint32_t n_walks, uint32_t B, int64_t* out_dev,
+                void* cuda_stream);
+int sched_walks_host(int32_t kind, int64_t n, double mu, int64_t n_prev, double p,
+                     uint64_t seed, uint64_t walk_begin, uint32_t n_walks, uint32_t B,
+                     int64_t* out_host, int32_t device);
+
 void sched_destroy(sched_t h);
 const char* sched_last_error(void);
 

@@ -21,6 +21,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "des_oracle.cpp")
+_SRC_WALKS = os.path.join(_HERE, "walks_oracle.cpp")
 
 FIELDS = [
     "arrivals", "admitted", "completed", "completed_after_T", "completed_tokens",
@@ -38,9 +39,10 @@ WAIT, NESTED, FCFS, FCFS_ONGOING = 0, 1, 2, 3
 def build(force: bool = False) -> str:
     """Compile liboracle.so (plain g++, no fast-math, no FMA contraction)."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
-            os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
+            os.path.getmtime(_SRC), os.path.getmtime(_SRC_WALKS),
+            os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
         subprocess.check_call(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fPIC",
-                               "-shared", "-o", _SO, _SRC, "-lpthread"])
+                               "-shared", "-o", _SO, _SRC, _SRC_WALKS, "-lpthread"])
     return _SO
 
 
@@ -75,6 +77,8 @@ def lib():
         _lib.orc_run_trace.argtypes = [C.POINTER(_Cfg), C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                        C.c_void_p, C.c_int64]
+        _lib.orc_walks.argtypes = [C.c_int32, C.c_int64, C.c_double, C.c_int64, C.c_double,
+                                   C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p]
         _lib.orc_gen_arrivals.argtypes = [C.POINTER(_Cfg), C.c_uint64, C.c_uint32,
                                           C.c_int32, C.c_int64, C.c_void_p, C.c_void_p,
                                           C.c_void_p]
@@ -199,3 +203,15 @@ def u128(rows: np.ndarray, name: str) -> List[int]:
     lo = rows[F[name + "_lo"]].astype(object)
     hi = rows[F[name + "_hi"]].astype(object)
     return [int(h) << 64 | int(x) for x, h in zip(lo, hi)]
+
+
+WALK_FIELDS = ["W_B", "stuck", "sumW", "maxW", "Wt_B", "viol", "sumX", "maxS", "minS", "S_B"]
+WF = {n: i for i, n in enumerate(WALK_FIELDS)}
+
+
+def walks(kind: int, n: int, B: int, n_walks: int, seed: int, walk_begin: int = 0,
+          mu: float = 0.0, n_prev: int = 0, p: float = 0.0) -> np.ndarray:
+    """Appendix random-walk chains, field-major [10, n_walks]."""
+    out = np.zeros((len(WALK_FIELDS), n_walks), dtype=np.int64)
+    lib().orc_walks(kind, n, mu, n_prev, p, seed, walk_begin, n_walks, B, out.ctypes.data)
+    return out

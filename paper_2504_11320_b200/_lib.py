@@ -31,7 +31,10 @@ F = {n: i for i, n in enumerate(FIELDS)}
 
 # every symbol include/sched.h declares
 EXPORTS = ["sched_create", "sched_thresholds", "sched_run", "sched_run_host",
-           "sched_run_trace", "sched_get_launch_info", "sched_destroy", "sched_last_error"]
+           "sched_run_trace", "sched_get_launch_info", "sched_walks", "sched_walks_host",
+           "sched_destroy", "sched_last_error"]
+WALK_FIELDS = ["W_B", "stuck", "sumW", "maxW", "Wt_B", "viol", "sumX", "maxS", "minS", "S_B"]
+WF = {n: i for i, n in enumerate(WALK_FIELDS)}
 
 
 class SchedError(RuntimeError):
@@ -102,8 +105,15 @@ def lib() -> C.CDLL:
                                       C.c_int64, C.POINTER(C.c_int64)]
         L.sched_get_launch_info.argtypes = [C.c_void_p, C.POINTER(LaunchInfo)]
         L.sched_destroy.argtypes = [C.c_void_p]
+        L.sched_walks.argtypes = [C.c_int32, C.c_int64, C.c_double, C.c_int64, C.c_double,
+                                  C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p,
+                                  C.c_void_p]
+        L.sched_walks_host.argtypes = [C.c_int32, C.c_int64, C.c_double, C.c_int64, C.c_double,
+                                       C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p,
+                                       C.c_int32]
         for name in ["sched_create", "sched_thresholds", "sched_run", "sched_run_host",
-                     "sched_run_trace", "sched_get_launch_info"]:
+                     "sched_run_trace", "sched_get_launch_info", "sched_walks",
+                     "sched_walks_host"]:
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -253,3 +263,21 @@ def u128(rows: np.ndarray, name: str):
     lo = rows[F[name + "_lo"]]
     hi = rows[F[name + "_hi"]]
     return [int(h) << 64 | int(x) for x, h in zip(lo, hi)]
+
+
+def walks(kind: int, n: int, B: int, n_walks: int, seed: int, walk_begin: int = 0,
+          mu: float = 0.0, n_prev: int = 0, p: float = 0.0, device: int = 0) -> np.ndarray:
+    """Appendix random-walk chains on the GPU (C ABI sched_walks_host):
+    field-major int64 [len(WALK_FIELDS), n_walks]."""
+    out = np.zeros((len(WALK_FIELDS), n_walks), dtype=np.int64)
+    _check(lib().sched_walks_host(kind, n, mu, n_prev, p, seed, walk_begin, n_walks, B,
+                                  out.ctypes.data, device))
+    return out
+
+
+def walks_device(kind: int, n: int, B: int, n_walks: int, seed: int, out_ptr: int,
+                 walk_begin: int = 0, mu: float = 0.0, n_prev: int = 0, p: float = 0.0,
+                 stream_ptr: int = 0):
+    """Asynchronous launch into a device buffer of len(WALK_FIELDS) * n_walks int64."""
+    _check(lib().sched_walks(kind, n, mu, n_prev, p, seed, walk_begin, n_walks, B,
+                             C.c_void_p(out_ptr), C.c_void_p(stream_ptr)))

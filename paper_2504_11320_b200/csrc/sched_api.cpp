@@ -13,6 +13,7 @@
 #include "../../include/sched.h"
 #include "setup.h"
 #include "sim_internal.h"
+#include "walks.h"
 
 using namespace waitsim;
 
@@ -594,6 +595,54 @@ int sched_get_launch_info(sched_t h, sched_launch_info* out) {
   out->spec_resident = (int32_t)h->Rc;
   out->fallback_grid = h->fallback ? h->fb_grid : 0;
   out->fallback_warps_per_block = h->fallback ? h->fb_wpb : 0;
+  return SCHED_OK;
+}
+
+static int walk_params(int32_t kind, int64_t n, double mu, int64_t n_prev, double p, uint64_t seed,
+                       uint64_t walk_begin, uint32_t n_walks, uint32_t B, WalkParams* w) {
+  if (kind != 0 && kind != 1) return fail(SCHED_E_INVALID, "walk kind must be 0 or 1");
+  if (n < 1 || n_walks == 0 || B == 0) return fail(SCHED_E_INVALID, "need n >= 1, n_walks > 0, B > 0");
+  if (walk_begin + n_walks > (1ull << 32)) return fail(SCHED_E_INVALID, "walk index exceeds 2^32");
+  if (kind == 0 && !(mu > 0 && mu <= 1e4)) return fail(SCHED_E_INVALID, "need 0 < mu <= 1e4");
+  if (kind == 1 && (n_prev < 1 || !(p > 0 && p < 1))) return fail(SCHED_E_INVALID, "need n_prev >= 1, 0 < p < 1");
+  *w = WalkParams{};
+  w->kind = kind; w->n = n; w->seed = seed; w->walk_begin = walk_begin; w->n_walks = n_walks; w->B = B;
+  if (kind == 0) {
+    w->mu = mu;
+    w->p0 = std::exp(-mu);
+    w->kmax = (int64_t)(mu + 40.0 * std::sqrt(mu) + 100.0);
+  } else {
+    w->n_prev = n_prev;
+    w->p0 = std::pow(1.0 - p, (double)n_prev);
+    w->ratio = p / (1.0 - p);
+  }
+  return 0;
+}
+
+int sched_walks(int32_t kind, int64_t n, double mu, int64_t n_prev, double p, uint64_t seed,
+                uint64_t walk_begin, uint32_t n_walks, uint32_t B, int64_t* out_dev, void* cuda_stream) {
+  if (!out_dev) return fail(SCHED_E_INVALID, "null output");
+  WalkParams w;
+  if (int rc = walk_params(kind, n, mu, n_prev, p, seed, walk_begin, n_walks, B, &w)) return rc;
+  w.out = out_dev;
+  CK(launch_walks(w, (cudaStream_t)cuda_stream));
+  return SCHED_OK;
+}
+
+int sched_walks_host(int32_t kind, int64_t n, double mu, int64_t n_prev, double p, uint64_t seed,
+                     uint64_t walk_begin, uint32_t n_walks, uint32_t B, int64_t* out_host, int32_t device) {
+  if (!out_host) return fail(SCHED_E_INVALID, "null output");
+  WalkParams w;
+  if (int rc = walk_params(kind, n, mu, n_prev, p, seed, walk_begin, n_walks, B, &w)) return rc;
+  CK(cudaSetDevice(device));
+  const size_t bytes = (size_t)kWalkFields * n_walks * 8;
+  int64_t* d = nullptr;
+  CK(cudaMalloc(&d, bytes));
+  w.out = d;
+  cudaError_t e = launch_walks(w, 0);
+  if (e == cudaSuccess) e = cudaMemcpy(out_host, d, bytes, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(e, "sched_walks_host");
   return SCHED_OK;
 }
 
