@@ -120,3 +120,43 @@ def main(argv=None):
 
 if __name__ == "__main__":
     main(sys.argv[1:])
+
+
+# --------------------------------------------------- Thm 1 zeta-sweep (NEXT(4))
+def zeta_sweep(zetas=(1, 2, 4, 8, 16), reps: int = 4096, slack: bool = True, device: int = 0):
+    """Asymptotic regime of Thm 1: scale arrival rates
+    by zeta and the batch-time coefficients by 1/zeta (C fixed).  WAIT with
+    the fluid-integer thresholds of the zeta = 1 system.  Reports per zeta the
+    throughput gap Throughput* - E[Throughput] (in tokens per unscaled second,
+    i.e. divided by zeta) and mean latency / TTFT (times zeta): Thm 1 gives a
+    gap O((zeta T)^-1) and O(1) latency under strict slack (dT < n_j/lambda_j),
+    O((zeta T)^-1/2) and O((zeta T)^1/2) at equality."""
+    import numpy as np
+    import workloads as W
+    from . import F, Scheduler, u128
+    base = W.C1P if slack else W.Workload("C1eq", [74.0], [W.fixed(8)], [W.fixed(16)], M=272,
+                                          horizon_s=W.C1P.horizon_s, seed=W.seed_for(11),
+                                          d0_s=1.0 / 74.0 - W.D1_S * 272)
+    out = []
+    # at equality the recipe would round to n = 2 (M^pi > M); Thm 1's
+    # equality case is n = 1 with dT(n) = n / lambda
+    thr = None if slack else [1]
+    for z in zetas:
+        wl = W.Workload(f"{base.name}_z{z}", [x * z for x in base.lam], base.l_tab, base.lp_tab,
+                        M=base.M, horizon_s=base.horizon_s, seed=base.seed,
+                        d0_s=base.d0_s / z, d1_s=base.d1_s / z)
+        s = Scheduler(wl, W.Policy(W.WAIT), thr, device=device)
+        rep = s.thresholds()
+        if thr is None:
+            thr = rep["thresholds"]
+        rows = s.run_host(wl.seed, 0, reps, wl.horizon_s)
+        T = wl.horizon_s
+        thr_tok = rows[F["completed_tokens"]].astype(float) / T
+        lat = np.array(u128(rows, "lat"), float) / 1e12 / np.maximum(rows[F["completed"]], 1)
+        ttft = np.array(u128(rows, "ttft"), float) / 1e12 / np.maximum(rows[F["first_tokens"]], 1)
+        gap = (rep["thr_star"] - thr_tok) / z
+        out.append(dict(zeta=z, thresholds=thr, dT_n=rep["dT_n"], slack=1.0 / 74.0 - rep["dT_n"] * z,
+                        gap=float(gap.mean()), gap_se=float(gap.std(ddof=1) / np.sqrt(reps)),
+                        latency=float((lat * z).mean()), ttft=float((ttft * z).mean()),
+                        evictions=int(rows[F["evictions"]].sum())))
+    return out

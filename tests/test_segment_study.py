@@ -50,3 +50,32 @@ def test_simulated_peaks_respect_bound(L):
     peaks, rows = studies.simulate_peaks(50.0, 200.0, L, r["thresholds"], 512)
     frac = float((peaks > r["total"]).mean())
     assert frac <= 0.1 + 3 * math.sqrt(0.1 * 0.9 / 512)
+
+
+@pytest.mark.gpu
+def test_thm1_zeta_sweep_strict_slack():
+    """Thm 1 under strict slack: the zeta-normalised
+    throughput gap shrinks ~ 1/zeta (faster than zeta^-1/2) and the
+    zeta-normalised latency stays O(1)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    rows = studies.zeta_sweep(zetas=(1, 4, 16), reps=2048)
+    g1, g4, g16 = (r["gap"] for r in rows)
+    assert g16 < g1 / 4 ** 0.5 * 0.5          # much faster than the zeta^-1/2 rate
+    lat = [r["latency"] for r in rows]
+    assert max(lat) < 1.5 * min(lat)
+    assert all(r["evictions"] == 0 for r in rows)
+
+
+@pytest.mark.gpu
+def test_thm1_zeta_sweep_equality():
+    """Thm 1 at equality dT(n) = n/lambda: gap O((zeta T)^-1/2), latency
+    O((zeta T)^1/2) -- the gap falls roughly like zeta^-1/2 and latency grows."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    rows = studies.zeta_sweep(zetas=(1, 16), reps=2048, slack=False)
+    ratio = rows[1]["gap"] / rows[0]["gap"]
+    assert 1 / 16 < ratio < 1 / 2          # between the 1/zeta and flat rates; ~ zeta^-1/2 = 1/4
+    assert rows[1]["latency"] > 1.5 * rows[0]["latency"]
