@@ -157,6 +157,80 @@ struct __align__(16) WarpStats {
   int64_t busy, idle, max_kv, log_n;
 };
 
+// arrival tick at operational time tau of a time-varying class: invert the
+// integrated piecewise-constant rate
+__device__ __forceinline__ int64_t tv_tick_at(const int64_t* rf_B, const int64_t* rf_Lam,
+                                              const double* rf_scale, uint32_t off, uint32_t n,
+                                              int64_t tau) {
+  uint32_t lo = 0, hi = n;  // largest p with Lam[p] <= tau (Lam[0] = 0)
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(rf_Lam + off + mid) <= tau) lo = mid; else hi = mid;
+  }
+  const double scale = __ldg(rf_scale + off + lo);
+  if (scale == 0.0) return TMAX;
+  int64_t t = __ldg(rf_B + off + lo) +
+              __double2ll_rz(__dmul_rn(__ll2double_rn(tau - __ldg(rf_Lam + off + lo)), scale));
+  if (lo + 1 < n) t = min(t, __ldg(rf_B + off + lo + 1) - 1);
+  return t;
+}
+
+// S1 arrival generation, one warp: lane i draws
+// arrival base+i of class c from Philox counter (k, r, c, 0), the gaps (or
+// operational-time increments) become ticks by an inclusive warp scan on top
+// of `prev`, marks by inverse CDF.  Not inlined: one copy per kernel keeps
+// the instruction footprint small (called at most once per 32 arrivals).
+__device__ __forceinline__ void gen_window_impl(int lane, uint32_t base, int64_t prev, uint32_t rglob,
+                                        uint32_t c, uint64_t seed, double gs,
+                                        const uint64_t* __restrict__ cdf_thr,
+                                        const uint16_t* __restrict__ cdf_val, uint32_t l_off,
+                                        uint32_t l_n, uint32_t lp_off, uint32_t lp_n,
+                                        uint32_t rf_off, uint32_t rf_n, const int64_t* rf_B,
+                                        const int64_t* rf_Lam, const double* rf_scale,
+                                        int64_t* wt, uint16_t* wl, uint16_t* wlp, int64_t* wtau) {
+  const uint32_t k = base + (uint32_t)lane;
+  int64_t t = TMAX, tau = 0;
+  uint32_t l = 1, lp = 1;
+  if (gs != 0.0 || rf_n != 0) {
+    uint32_t x0, x1, x2, x3;
+    philox4x32_10(k, rglob, c, 0u, (uint32_t)seed, (uint32_t)(seed >> 32), x0, x1, x2, x3);
+    const double E = neglog_bits(x0, x1);
+    if (rf_n != 0) {
+      // time change: tau_k = tau_{k-1} + (int64)(E 2^32), t_k = Lambda^{-1}(tau_k)
+      tau = prev + warp_incl_scan_i64(__double2ll_rz(__dmul_rn(E, 4294967296.0)), lane);
+      t = tv_tick_at(rf_B, rf_Lam, rf_scale, rf_off, rf_n, tau);
+    } else {
+      t = prev + warp_incl_scan_i64(__double2ll_rz(__dmul_rn(E, gs)), lane);
+    }
+    l = cdf_sample(cdf_thr, cdf_val, l_off, l_n, x2);
+    lp = cdf_sample(cdf_thr, cdf_val, lp_off, lp_n, x3);
+  }
+  __syncwarp();
+  wt[lane] = t;
+  wl[lane] = (uint16_t)l;
+  wlp[lane] = (uint16_t)lp;
+  if (wtau) wtau[lane] = tau;
+  __syncwarp();
+}
+
+#define GEN_WINDOW_ARGS                                                                      \
+  int lane, uint32_t base, int64_t prev, uint32_t rglob, uint32_t c, uint64_t seed, double gs, \
+      const uint64_t *cdf_thr, const uint16_t *cdf_val, uint32_t l_off, uint32_t l_n,         \
+      uint32_t lp_off, uint32_t lp_n, uint32_t rf_off, uint32_t rf_n, const int64_t *rf_B,    \
+      const int64_t *rf_Lam, const double *rf_scale, int64_t *wt, uint16_t *wl, uint16_t *wlp, \
+      int64_t *wtau
+#define GEN_WINDOW_PASS                                                                   \
+  lane, base, prev, rglob, c, seed, gs, cdf_thr, cdf_val, l_off, l_n, lp_off, lp_n, rf_off, \
+      rf_n, rf_B, rf_Lam, rf_scale, wt, wl, wlp, wtau
+// one out-of-line copy (large kernels: instruction-cache footprint) ...
+__device__ __noinline__ void gen_window_call(GEN_WINDOW_ARGS) { gen_window_impl(GEN_WINDOW_PASS); }
+// ... or inlined (WAIT: register-bound, a call costs spills)
+template <bool INLINE>
+__device__ __forceinline__ void gen_window(GEN_WINDOW_ARGS) {
+  if (INLINE) gen_window_impl(GEN_WINDOW_PASS);
+  else gen_window_call(GEN_WINDOW_PASS);
+}
+
 template <int POL, bool TRACE>
 struct WarpSim {
   const DevParams& P;
@@ -246,67 +320,35 @@ struct WarpSim {
   // turned into ticks by an inclusive warp scan on top of `prev`.
   __device__ __forceinline__ bool is_tv(int c) const { return !TRACE && P.cls[c].rf_n != 0; }
 
-  // arrival tick at operational time tau of a time-varying class: invert the
-  // integrated piecewise-constant rate
-  __device__ __forceinline__ int64_t tv_tick(int c, int64_t tau) const {
-    const uint32_t off = P.cls[c].rf_off, n = P.cls[c].rf_n;
-    uint32_t lo = 0, hi = n;  // largest p with Lam[p] <= tau (Lam[0] = 0)
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (__ldg(P.rf_Lam + off + mid) <= tau) lo = mid; else hi = mid;
-    }
-    const double scale = __ldg(P.rf_scale + off + lo);
-    if (scale == 0.0) return TMAX;
-    int64_t t = __ldg(P.rf_B + off + lo) +
-                __double2ll_rz(__dmul_rn(__ll2double_rn(tau - __ldg(P.rf_Lam + off + lo)), scale));
-    if (lo + 1 < n) t = min(t, __ldg(P.rf_B + off + lo + 1) - 1);
-    return t;
-  }
 
+  // S1 window fill: 32 arrivals [base, base+32) of class c into (wt, wl, wlp)
+  // (+ operational time for time-varying classes).  Philox mode calls the
+  // single non-inlined generator below; trace mode reads the explicit trace.
   template <bool WITH_LEN>
   __device__ __forceinline__ void fill(int c, uint32_t base, int64_t prev, int64_t* wt,
                                        uint16_t* wl, uint16_t* wlp) {
-    const uint32_t k = base + lane;
-    int64_t t, tau = 0;
-    uint32_t l = 1, lp = 1;
     const bool tv = is_tv(c);
+    int64_t* wtau = tv ? (wt == vt ? vtau : atau) : nullptr;
     if (TRACE) {
+      const uint32_t k = base + lane;
       const int64_t beg = P.tr_off[(size_t)rep * P.K + c];
       const int64_t end = P.tr_off[(size_t)rep * P.K + c + 1];
+      int64_t t = TMAX;
+      uint32_t l = 1, lp = 1;
       if (beg + (int64_t)k < end) {
         t = P.tr_t[beg + k];
         if (WITH_LEN) { l = P.tr_l[beg + k]; lp = P.tr_lp[beg + k]; }
-      } else {
-        t = TMAX;
       }
-    } else {
-      const double gs = P.cls[c].gap_scale;
-      if (gs == 0.0 && !tv) {
-        t = TMAX;
-      } else {
-        uint32_t x0, x1, x2, x3;
-        philox4x32_10(k, rglob, (uint32_t)c, 0u, (uint32_t)P.seed, (uint32_t)(P.seed >> 32),
-                      x0, x1, x2, x3);
-        if (tv) {
-          // time change: tau_k = tau_{k-1} + (int64)(E 2^32), t_k = Lambda^{-1}(tau_k)
-          const int64_t g = __double2ll_rz(__dmul_rn(neglog_bits(x0, x1), 4294967296.0));
-          tau = prev + warp_incl_scan_i64(g, lane);
-          t = tv_tick(c, tau);
-        } else {
-          const int64_t gap = __double2ll_rz(__dmul_rn(neglog_bits(x0, x1), gs));
-          t = prev + warp_incl_scan_i64(gap, lane);
-        }
-        if (WITH_LEN) {
-          l = cdf_sample(P.cdf_thr, P.cdf_val, P.cls[c].l_off, P.cls[c].l_n, x2);
-          lp = cdf_sample(P.cdf_thr, P.cdf_val, P.cls[c].lp_off, P.cls[c].lp_n, x3);
-        }
-      }
+      __syncwarp();
+      wt[c * 32 + lane] = t;
+      if (WITH_LEN) { wl[c * 32 + lane] = (uint16_t)l; wlp[c * 32 + lane] = (uint16_t)lp; }
+      __syncwarp();
+      return;
     }
-    __syncwarp();
-    wt[c * 32 + lane] = t;
-    if (WITH_LEN) { wl[c * 32 + lane] = (uint16_t)l; wlp[c * 32 + lane] = (uint16_t)lp; }
-    if (tv) (wt == vt ? vtau : atau)[c * 32 + lane] = tau;
-    __syncwarp();
+    const ClassParam& cp = P.cls[c];
+    gen_window<POL == SCHED_WAIT>(lane, base, prev, rglob, (uint32_t)c, P.seed, cp.gap_scale, P.cdf_thr, P.cdf_val,
+               cp.l_off, cp.l_n, cp.lp_off, cp.lp_n, cp.rf_off, cp.rf_n, P.rf_B, P.rf_Lam,
+               P.rf_scale, wt + c * 32, wl + c * 32, wlp + c * 32, wtau ? wtau + c * 32 : nullptr);
   }
 
   // class-c cursor fields (uniform broadcast from lane c)
