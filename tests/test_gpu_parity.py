@@ -274,3 +274,33 @@ def test_full_size_bench_config_sampled():
                 + f("final_resident")).all()
         assert (got[oracle.F["max_kv_peak"]] <= W.C2.M).all()
         s.close()
+
+
+# ------------------------------------------------------------- edge cases
+def test_many_classes_and_zero_rates():
+    """K = 12 classes (some with rate 0), variable length tables."""
+    rng = np.random.default_rng(42)
+    lam, lt, lpt = [], [], []
+    for c in range(12):
+        lam.append(0.0 if c % 5 == 3 else float(rng.choice([10.0, 40.0, 90.0])))
+        lt.append(W.fixed(int(rng.integers(1, 6))) if c % 2 else [(2, 3), (4, 1), (7, 2)])
+        lpt.append(W.fixed(int(rng.integers(1, 8))) if c % 3 else [(1, 5), (3, 2), (9, 1)])
+    wl = W.Workload("k12", lam, lt, lpt, M=120, horizon_s=1.0, seed=77, d0_s=0.004, d1_s=2e-4)
+    check(wl, W.Policy(W.WAIT), [int(x) for x in rng.integers(1, 4, 12)], 16)
+    check(wl, W.Policy(W.FCFS, B=40), [0], 16)
+    check(wl, W.Policy(W.FCFS_ONGOING, B=40, tok_budget=20), [0], 16)
+    check(wl, W.Policy(W.NESTED, seg_end=[2, 5, 9]), [4, 3, 2], 16)
+
+
+def test_degenerate_horizons_and_capacity():
+    """No arrival before T; M = l + l' exactly (one prompt fits); all rates 0."""
+    tiny = W.Workload("tiny", [0.5], [W.fixed(3)], [W.fixed(4)], M=7, horizon_s=0.01, seed=5)
+    for pol, thr in [(W.Policy(W.WAIT), [1]), (W.Policy(W.FCFS, B=4), [0]),
+                     (W.Policy(W.NESTED, seg_end=[4]), [1])]:
+        check(tiny, pol, thr, 8)
+        check(W.Workload("m", [50.0], [W.fixed(3)], [W.fixed(4)], M=7, horizon_s=1.0, seed=6),
+              pol, thr, 8)
+    zero = W.Workload("zero", [0.0, 0.0], [W.fixed(1)] * 2, [W.fixed(1)] * 2, M=10,
+                      horizon_s=1.0, seed=1)
+    rows = check(zero, W.Policy(W.FCFS, B=2), [0], 4)
+    assert (rows[oracle.F["arrivals"]] == 0).all()
