@@ -133,7 +133,12 @@ __device__ __forceinline__ uint32_t bcast32(uint32_t v, int src) { return __shfl
 __device__ __forceinline__ uint64_t pack_q(uint32_t l, uint32_t lp, uint32_t s, uint32_t meta) {
   return (uint64_t)l | ((uint64_t)lp << 16) | ((uint64_t)s << 32) | ((uint64_t)meta << 48);
 }
-constexpr uint32_t META_RESTART = 0x200;  // staging mark: came from a restart ring
+constexpr uint32_t META_RESTART = 0x200;
+// one resident: arrival tick + packed record, 16 B (one LDS.128 / STS.128)
+struct __align__(16) Rec {
+  int64_t a;
+  uint64_t q;
+};  // staging mark: came from a restart ring
 
 // # of leading entries of the sorted array v[0..n) that precede `key`
 // (v <= key if le, v < key otherwise)
@@ -236,8 +241,7 @@ struct WarpSim {
   const DevParams& P;
   const int lane;
   // shared-memory views (this warp's slice)
-  int64_t* ra;                       // [Rc] arrival tick of each resident
-  uint64_t* rq;                      // [Rc] packed (l, l', s, meta)
+  Rec* rr;                           // [Rc] residents in admission order
   int64_t* vt;                       // [K][32] generated window (t): visibility + admission
   uint16_t* vl; uint16_t* vlp;       // [K][32] generated window (l, l')
   int64_t* at;                       // [K][32] private admission windows (t)
@@ -278,9 +282,8 @@ struct WarpSim {
   __device__ WarpSim(const DevParams& p, unsigned char* base, int lane_, size_t rb)
       : P(p), lane(lane_), ring_base(rb) {
     const uint32_t Rc = p.Rc;
-    ra = (int64_t*)base;
-    rq = (uint64_t*)(ra + Rc);
-    vt = (int64_t*)(rq + Rc);
+    rr = (Rec*)base;
+    vt = (int64_t*)(rr + Rc);
     at = vt + p.K * 32;
     re = at + p.K * 32;
     al = (uint16_t*)(re + 32);
@@ -437,11 +440,123 @@ struct WarpSim {
   // number of candidates before it (binary searches over the other sources'
   // windows); FCFS additionally cuts at the first prompt failing the
   // admission test (reading R15).
+  // FCFS admission cut: lane i holds staged candidate i (prefill length l);
+  // the longest prefix passing the test of PAPER.md:1427, 1745 (R15)
+  __device__ __forceinline__ uint32_t fcfs_take(uint32_t m, uint32_t l) const {
+    const uint32_t pre = warp_incl_scan_u32(l, lane);
+    const bool ok = (uint32_t)lane < m && (n_res + n_new + lane < P.B) &&
+                    // Sarathi-style ongoing-first also reserves the residents' growth (R29)
+                    (KV + (POL == SCHED_FCFS_ONGOING ? (int64_t)n_res : 0) + sum_new_l +
+                         (int64_t)pre <= P.M) &&
+                    (P.tok_budget == 0 || sum_new_l + (int64_t)pre <= (int64_t)P.tok_budget);
+    const uint32_t okm = __ballot_sync(FULL, ok);  // ok lanes form a prefix
+    return okm == FULL ? 32u : (uint32_t)__ffs(~okm) - 1;
+  }
+
+  // take_fifo fast path, one source class c (WAIT, or a single class): the
+  // FIFO head is arrivals k_adm .. of class c, read in order from its window
+  template <bool FCFS_COND>
+  __device__ __forceinline__ bool take_single(int c, uint32_t pend, uint32_t& want) {
+    const uint32_t p = bcast32(pend, c);
+    const uint32_t o = bcast32(k_adm - vbase, c);  // unused if p == 0
+    const uint32_t base = n_res + n_new;
+    uint32_t m = min(p, want);
+    if (FCFS_COND) m = min(m, P.B > base ? P.B - base : 0u);
+    if (m == 0) return true;
+    if (base + m > P.Rc) { status = 1; return false; }
+    uint32_t l = 0;
+    if ((uint32_t)lane < m) {
+      const int idx = c * 32 + (int)(o + lane);
+      l = vl[idx];
+      rr[base + lane] = Rec{vt[idx], pack_q(l, vlp[idx], 1, (uint32_t)c)};
+    }
+    const uint32_t take = FCFS_COND ? fcfs_take(m, l) : m;
+    if (lane == c) { k_adm += take; newc += take; }
+    n_new += take;
+    sum_new_l += __reduce_add_sync(FULL, (uint32_t)lane < take ? l : 0u);
+    want -= take;
+    __syncwarp();
+    return true;
+  }
+
+  // take_fifo fast path, several classes merged by (t, class): candidate g
+  // of class s ranks pos + #(earlier arrivals of the other classes), by
+  // binary search over their windows.  Returns -1 capacity error, 0 done,
+  // 1 took a full chunk (more may follow).
+  template <bool FCFS_COND>
+  __device__ __forceinline__ int take_merged(uint32_t pend, uint32_t& want) {
+    const uint32_t my_o = pend ? k_adm - vbase : 0u;
+    const uint32_t incl = warp_incl_scan_u32(pend, lane);  // lanes >= K: pend = 0
+    const uint32_t ncand = __shfl_sync(FULL, incl, 31);
+    if (ncand == 0) return 0;
+    const uint32_t base = n_res + n_new;
+    uint32_t m = min(min(ncand, 32u), want);
+    if (FCFS_COND) m = min(m, P.B > base ? P.B - base : 0u);
+    if (m == 0) return 0;
+    if (base + m > P.Rc) { status = 1; return -1; }
+    const int K = P.K;
+    for (uint32_t g0 = 0; g0 < ncand; g0 += 32) {
+      const uint32_t g = g0 + (uint32_t)lane;
+      const bool act = g < ncand;
+      int s = 0;  // source class: first class whose candidate range ends after g
+      for (int c = 0; c < K; ++c) s += bcast32(incl, c) <= g;
+      s = min(s, K - 1);
+      const uint32_t s_n = __shfl_sync(FULL, pend, s), s_o = __shfl_sync(FULL, my_o, s);
+      const uint32_t pos = g - (__shfl_sync(FULL, incl, s) - s_n);
+      const int idx = s * 32 + (int)(s_o + pos);
+      const int64_t t = act ? vt[idx] : 0;
+      uint32_t r = pos;
+      for (int c = 0; c < K; ++c) {
+        const uint32_t n = bcast32(pend, c), o = bcast32(my_o, c);
+        // ties: a lower class index precedes
+        if (act && c != s && n) r += count_before(vt + c * 32 + o, n, t, c < s);
+      }
+      if (act && r < m) {
+        rr[base + r] = Rec{t, pack_q(vl[idx], vlp[idx], 1, (uint32_t)s)};
+      }
+    }
+    __syncwarp();
+    uint64_t qv = 0;
+    uint32_t l = 0;
+    if ((uint32_t)lane < m) { qv = rr[base + lane].q; l = (uint32_t)(qv & 0xFFFF); }
+    const uint32_t take = FCFS_COND ? fcfs_take(m, l) : min(m, want);
+    if (take == 0) return 0;
+    const bool tk = (uint32_t)lane < take;
+    const uint32_t cls = (uint32_t)(qv >> 48) & 0xFF;
+    for (int c = 0; c < K; ++c) {
+      const uint32_t cc = __popc(__ballot_sync(FULL, tk && cls == (uint32_t)c));
+      if (lane == c) { k_adm += cc; newc += cc; }
+    }
+    n_new += take;
+    sum_new_l += __reduce_add_sync(FULL, tk ? l : 0u);
+    want -= take;
+    __syncwarp();
+    return take < m ? 0 : 1;
+  }
+
   template <bool FCFS_COND>
   __device__ bool take_fifo(int q, uint32_t want) {
     const int c_lo = POL == SCHED_WAIT ? q : 0;
     const int c_hi = POL == SCHED_WAIT ? q + 1 : P.K;
     while (want > 0) {
+      // fast path (the common case): no restart waits in FIFO q and every
+      // class's waiting arrivals sit in its generated window (backlog <= 32,
+      // "attached"); lane c already holds class c's cursors
+      {
+        const bool in_rng = lane >= c_lo && lane < c_hi;
+        const uint32_t pend = in_rng ? k_vis - k_adm : 0u;
+        const bool ok = (pend == 0 || k_adm >= vbase) && (lane != q || rtail == rhead);
+        if (__all_sync(FULL, ok)) {
+          if (c_hi - c_lo == 1) {
+            if (!take_single<FCFS_COND>(c_lo, pend, want)) return false;
+            break;
+          }
+          const int r = take_merged<FCFS_COND>(pend, want);
+          if (r < 0) return false;
+          if (r == 0) break;
+          continue;
+        }
+      }
       // (1) each class's candidate window = its first min(pending, 32)
       // waiting arrivals, as up to two sorted segments: private window part
       // (or the generated window when attached) + the generated window
@@ -543,28 +658,15 @@ struct WarpSim {
           }
         }
         if (act && r < m) {
-          ra[base + r] = a;
-          rq[base + r] = pack_q(l, lp, 1, meta);
+          rr[base + r] = Rec{a, pack_q(l, lp, 1, meta)};
         }
       }
       __syncwarp();
       // (3) how many to take
       uint64_t qv = 0;
       uint32_t l = 0;
-      if ((uint32_t)lane < m) { qv = rq[base + lane]; l = (uint32_t)(qv & 0xFFFF); }
-      uint32_t take;
-      if (FCFS_COND) {
-        const uint32_t pre = warp_incl_scan_u32(l, lane);
-        const bool ok = (uint32_t)lane < m && (n_res + n_new + lane < P.B) &&
-                        // Sarathi-style ongoing-first also reserves the residents' growth (R29)
-                        (KV + (POL == SCHED_FCFS_ONGOING ? (int64_t)n_res : 0) + sum_new_l +
-                             (int64_t)pre <= P.M) &&
-                        (P.tok_budget == 0 || sum_new_l + (int64_t)pre <= (int64_t)P.tok_budget);
-        const uint32_t okm = __ballot_sync(FULL, ok);  // ok lanes form a prefix
-        take = okm == FULL ? 32u : (uint32_t)__ffs(~okm) - 1;
-      } else {
-        take = min(m, want);
-      }
+      if ((uint32_t)lane < m) { qv = rr[base + lane].q; l = (uint32_t)(qv & 0xFFFF); }
+      const uint32_t take = FCFS_COND ? fcfs_take(m, l) : min(m, want);
       if (take == 0) break;
       // (4) consume: advance each source's cursor by what it contributed
       const bool tk = (uint32_t)lane < take;
@@ -576,7 +678,7 @@ struct WarpSim {
       }
       const uint32_t crs = __popc(__ballot_sync(FULL, rst));
       if (lane == q) { rhead += crs; if (POL == SCHED_WAIT) newc += crs; }
-      if (rst) rq[base + lane] = qv & ~((uint64_t)META_RESTART << 48);
+      if (rst) rr[base + lane].q = qv & ~((uint64_t)META_RESTART << 48);
       n_new += take;
       sum_new_l += __reduce_add_sync(FULL, tk ? l : 0u);
       want -= take;
@@ -678,7 +780,7 @@ struct WarpSim {
       const bool valid = idx >= 0;
       uint64_t qv = 0;
       int64_t a = 0;
-      if (valid) { qv = rq[idx]; a = ra[idx]; }
+      if (valid) { const Rec e = rr[idx]; qv = e.q; a = e.a; }
       const uint32_t l = (uint32_t)(qv & 0xFFFF), lp = (uint32_t)((qv >> 16) & 0xFFFF);
       const uint32_t s = (uint32_t)((qv >> 32) & 0xFFFF), meta = (uint32_t)(qv >> 48);
       uint32_t inp = 0, nkey = 0;
@@ -745,18 +847,17 @@ struct WarpSim {
     if (n_res != old_n && n_new > 0) {
       for (uint32_t o = 0; o < n_new; o += 32) {
         const uint32_t i = o + lane;
-        int64_t a = 0;
-        uint64_t qv = 0;
-        if (i < n_new) { a = ra[old_n + i]; qv = rq[old_n + i]; }
+        Rec e = {0, 0};
+        if (i < n_new) e = rr[old_n + i];
         __syncwarp();
-        if (i < n_new) { ra[n_res + i] = a; rq[n_res + i] = qv; }
+        if (i < n_new) rr[n_res + i] = e;
         __syncwarp();
       }
     }
     if (excess > 0) {
       // no residents left: drop the latest new admissions (they stay queued)
       uint32_t keep = n_new;
-      while (excess > 0 && keep > 0) { excess -= (int64_t)(rq[n_res + keep - 1] & 0xFFFF); --keep; }
+      while (excess > 0 && keep > 0) { excess -= (int64_t)(rr[n_res + keep - 1].q & 0xFFFF); --keep; }
       restore_cursors();
       n_new = 0;
       sum_new_l = 0;
@@ -840,18 +941,43 @@ struct WarpSim {
     return u;
   }
 
-  // in-place stream compaction of one chunk (ballot + popc keeps order)
-  __device__ __forceinline__ void compact(const Upd& u, uint32_t i, int64_t a, uint64_t qv,
-                                          uint32_t& wp) {
+  // in-place stream compaction of one chunk (ballot + popc keeps order).
+  // No __syncwarp around the stores: every lane's load of this chunk feeds
+  // the ballot before any store, stores go to d <= i (slots this or earlier
+  // chunks already read), and the next chunk reads beyond them.
+  __device__ __forceinline__ void compact(const Upd& u, int64_t a, uint32_t& wp) {
     const uint32_t km = __ballot_sync(FULL, u.keep);
     const uint32_t d = wp + __popc(km & lanemask_lt());
-    __syncwarp();
-    if (u.keep) {
-      if (d != i) { ra[d] = a; rq[d] = pack_q(u.l, u.lp, u.ns, u.meta); }
-      else if (u.inp) rq[d] = pack_q(u.l, u.lp, u.ns, u.meta);
-    }
+    if (u.keep) rr[d] = Rec{a, pack_q(u.l, u.lp, u.ns, u.meta)};
     wp += __popc(km);
-    __syncwarp();
+  }
+
+  // WAIT / FCFS per-member step + compaction, branch-light: membership,
+  // first token (stage 1), completion after stage l'
+  // (frees l+l'-1) or s++
+  __device__ __forceinline__ void step_plain(uint32_t i, bool v, const Rec& e, Acc& acc, uint32_t& wp) {
+    const uint64_t q = e.q;
+    const uint32_t l = (uint32_t)(q & 0xFFFF), lp = (uint32_t)((q >> 16) & 0xFFFF);
+    const uint32_t s = (uint32_t)((q >> 32) & 0xFFFF), meta = (uint32_t)(q >> 48);
+    bool inp = v && i < n_res;  // staged admissions (i >= n_res) just keep stage 1
+    if (POL == SCHED_WAIT) inp = inp && ((Qmask >> (meta & 0xFF)) & 1u);
+    const bool ft = inp && s == 1 && !(meta & META_FT);
+    const bool done = inp && s == lp;
+    acc.tok += inp ? l + s : 0u;
+    acc.n_ft += ft;
+    acc.ft_a += ft ? (uint64_t)e.a : 0ull;
+    acc.n_done += done;
+    acc.done_tok += done ? lp : 0u;
+    acc.kv_free += done ? l + lp - 1 : 0u;
+    acc.done_a += done ? (uint64_t)e.a : 0ull;
+    acc.grow += inp && !done;
+    if (POL == SCHED_WAIT && done) atomicSub(&cnt[meta & 0xFF], 1u);
+    const uint64_t nq = q + ((inp && !done) ? (1ull << 32) : 0ull) + (ft ? ((uint64_t)META_FT << 48) : 0ull);
+    const bool keep = v && !done;
+    const uint32_t km = __ballot_sync(FULL, keep);
+    const uint32_t d = wp + __popc(km & lanemask_lt());
+    if (keep) rr[d] = Rec{e.a, nq};
+    wp += __popc(km);
   }
 
   // ------------------------------------------------------ S5 execute
@@ -867,33 +993,32 @@ struct WarpSim {
     }
     Acc acc;
     uint32_t wp = 0;
-    // two chunks per iteration: both chunks' loads issue before the first
-    // chunk's dependent chain (ILP); compaction stays in admission order
-    // (chunk 0's writes land below chunk 1's read positions)
-    if (POL == SCHED_WAIT) {  // register-bound at 20 warps/SM: one chunk at a time
-      for (uint32_t base = 0; base < n_tot; base += 32) {
-        const uint32_t i0 = base + lane;
-        const bool v0 = i0 < n_tot;
-        int64_t a0 = 0;
-        uint64_t q0 = 0;
-        if (v0) { a0 = ra[i0]; q0 = rq[i0]; }
-        const Upd u0 = member(v0, i0 >= n_res, a0, q0, over, acc);
-        compact(u0, i0, a0, q0, wp);
+    if (POL != SCHED_NESTED) {
+      // two chunks per iteration for ILP (chunk 0's stores land below chunk
+      // 1's slots, which were loaded first)
+      for (uint32_t base = 0; base < n_tot; base += 64) {
+        const uint32_t i0 = base + lane, i1 = i0 + 32;
+        const bool v0 = i0 < n_tot, v1 = i1 < n_tot;
+        Rec e0 = {0, 0}, e1 = {0, 0};
+        if (v0) e0 = rr[i0];
+        if (v1) e1 = rr[i1];
+        step_plain(i0, v0, e0, acc, wp);
+        if (base + 32 < n_tot) step_plain(i1, v1, e1, acc, wp);
       }
     } else {
       for (uint32_t base = 0; base < n_tot; base += 64) {
         const uint32_t i0 = base + lane, i1 = i0 + 32;
         const bool v0 = i0 < n_tot, v1 = i1 < n_tot;
-        int64_t a0 = 0, a1 = 0;
-        uint64_t q0 = 0, q1 = 0;
-        if (v0) { a0 = ra[i0]; q0 = rq[i0]; }
-        if (v1) { a1 = ra[i1]; q1 = rq[i1]; }
-        const Upd u0 = member(v0, i0 >= n_res, a0, q0, over, acc);
-        const Upd u1 = member(v1, i1 >= n_res, a1, q1, over, acc);
-        compact(u0, i0, a0, q0, wp);
-        compact(u1, i1, a1, q1, wp);
+        Rec e0 = {0, 0}, e1 = {0, 0};
+        if (v0) e0 = rr[i0];
+        if (v1) e1 = rr[i1];
+        const Upd u0 = member(v0, i0 >= n_res, e0.a, e0.q, over, acc);
+        const Upd u1 = member(v1, i1 >= n_res, e1.a, e1.q, over, acc);
+        compact(u0, e0.a, wp);
+        compact(u1, e1.a, wp);
       }
     }
+    __syncwarp();
     uint32_t tok = acc.tok, n_done = acc.n_done, done_tok = acc.done_tok, n_ft = acc.n_ft,
              kv_free = acc.kv_free, grow = acc.grow;
     const uint64_t done_a = acc.done_a, ft_a = acc.ft_a;
