@@ -191,6 +191,12 @@ typedef struct {
   int32_t max_resident, restart_cap;      /* safe capacity, ring capacity */
   int32_t spec_resident;                  /* main-launch capacity (== max_resident: no fallback) */
   int32_t fallback_grid, fallback_warps_per_block;
+  int32_t engine;                         /* 0 member engine (per-resident records, every
+                                             policy); 1 class-ring engine (WAIT / FCFS with
+                                             fixed per-class lengths; capacities
+                                             then count ring + staging records).  The env var
+                                             WAITSIM_ENGINE=member (read at the first run)
+                                             forces the member engine. */
 } sched_launch_info;
 int sched_get_launch_info(sched_t h, sched_launch_info* out);
 

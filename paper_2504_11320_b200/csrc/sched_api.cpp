@@ -17,6 +17,19 @@
 
 using namespace waitsim;
 
+// one launch configuration (engine + capacities + grid); the handle keeps one
+// for the member engine (every policy, explicit traces) and, when eligible,
+// one for the class-ring engine (sched_run of fixed-length WAIT / FCFS)
+struct LaunchCfg {
+  bool ring = false;
+  uint32_t Rc = 0, Rc_safe = 0;              // member: residents; ring: staging slots
+  uint32_t rcap[32] = {}, rcap_safe[32] = {};  // ring: per-class ring capacity
+  uint32_t warp_smem = 0, fb_warp_smem = 0;
+  int grid = 0, block = 0, wpb = 0, blocks_per_sm = 0;
+  int fb_grid = 0, fb_block = 0, fb_wpb = 0;
+  bool fallback = false;
+};
+
 namespace {
 thread_local std::string g_err;
 
@@ -62,12 +75,12 @@ struct sched_s {
   uint32_t* d_counter = nullptr;
   uint64_t* d_out = nullptr;
   size_t out_cap = 0;
-  // launch: main (speculative capacity Rc) and fallback (safe capacity Rc_safe)
-  int grid = 0, block = 0, wpb = 0, blocks_per_sm = 0, sm_count = 0;
-  uint32_t Rc = 0, warp_smem = 0;
-  int fb_grid = 0, fb_block = 0, fb_wpb = 0;
-  uint32_t Rc_safe = 0, fb_warp_smem = 0;
-  bool fallback = false;
+  // launch: main (speculative capacity) and fallback (safe capacity) per engine
+  int sm_count = 0;
+  LaunchCfg mem, rng;
+  bool use_ring = false;                     // sched_run uses the class-ring engine
+  double n_star_c[32] = {};                  // fluid prompts in service per class
+  double m_star = 0;                         // fluid KV occupancy M*
   uint32_t* d_retry = nullptr;
   size_t retry_cap = 0;
   double n_star_total = 0;  // fluid equilibrium prompts in service (0 = unknown)
@@ -168,23 +181,21 @@ int prepare(sched_s* h) {
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, h->device));
   h->sm_count = prop.multiProcessorCount;
-  if (is_fcfs(h->in.policy) && h->n_star_total == 0) {
+  const int K = (int)h->in.lambda.size();
+  if (h->n_star_total == 0 && h->in.policy != SCHED_NESTED) {
     sched_threshold_report rep;
     std::vector<uint32_t> ch;
     std::string err;
     try {
       if (compute_thresholds(h->in, 0, 0, 0, &rep, &ch, &err) == 0)
-        for (size_t c = 0; c < h->in.lambda.size() && c < 32; ++c) h->n_star_total += rep.n_star[c];
+        for (int c = 0; c < K && c < 32; ++c) { h->n_star_total += rep.n_star[c]; h->n_star_c[c] = rep.n_star[c]; }
+      h->m_star = rep.M_star;
     } catch (...) {
     }
   }
-  const int K = (int)h->in.lambda.size();
-  h->Rc_safe = derive_rc(h);
-  h->Rc = speculative_rc(h, h->Rc_safe);
-  h->fallback = h->Rc < h->Rc_safe;
   // choose warps per block maximising resident warps per SM
-  auto size_launch = [&](uint32_t Rc, uint32_t* wsm, int* wpb_out, int* bps_out) -> int {
-    *wsm = warp_smem_bytes(Rc, K, h->tv_any);
+  auto size_launch = [&](bool ring, uint32_t records, uint32_t* wsm, int* wpb_out, int* bps_out) -> int {
+    *wsm = warp_smem_bytes(records, K, h->tv_any, ring);
     int best_w = 0;
     const int cands[] = {8, 4, 2, 1};
     for (int wpb : cands) {
@@ -193,31 +204,102 @@ int prepare(sched_s* h) {
       if (smem > (size_t)prop.sharedMemPerBlockOptin) continue;
       // max blocks per SM from shared memory and registers (occupancy API)
       int bps = 0;
-      const cudaError_t e = sim_occupancy(h->in.policy, 0, wpb * 32, smem, &bps);
+      const cudaError_t e = sim_occupancy(h->in.policy, 0, wpb * 32, smem, &bps, ring ? 1 : 0);
       if (e != cudaSuccess) return cuda_fail(e, "occupancy");
       if (bps * wpb > best_w) { best_w = bps * wpb; *wpb_out = wpb; *bps_out = bps; }
     }
     if (best_w == 0)
-      return fail(SCHED_E_INVALID, "resident capacity too large for shared memory (max_resident=" +
-                                       std::to_string(Rc) + ")");
+      return fail(SCHED_E_INVALID, "resident capacity too large for shared memory (" +
+                                       std::to_string(records) + " records per replication)");
     return 0;
   };
-  int best_wpb = 1, best_bps = 0;
-  if (int rc = size_launch(h->Rc, &h->warp_smem, &best_wpb, &best_bps)) return rc;
-  h->wpb = best_wpb;
-  h->blocks_per_sm = best_bps;
-  h->block = best_wpb * 32;
-  h->grid = h->sm_count * best_bps;
-  h->fb_wpb = h->wpb; h->fb_block = h->block; h->fb_grid = 0; h->fb_warp_smem = h->warp_smem;
-  if (h->fallback) {
-    int fw = 1, fb = 0;
-    if (int rc = size_launch(h->Rc_safe, &h->fb_warp_smem, &fw, &fb)) return rc;
-    h->fb_wpb = fw;
-    h->fb_block = fw * 32;
-    h->fb_grid = h->sm_count * fb;
+  auto size_cfg = [&](LaunchCfg& L) -> int {
+    uint32_t rec = L.Rc, rec_safe = L.Rc_safe;
+    if (L.ring) {
+      rec += 32;  // eviction-round victim slots
+      rec_safe += 32;
+      for (int c = 0; c < K; ++c) { rec += L.rcap[c]; rec_safe += L.rcap_safe[c]; }
+    }
+    L.fallback = rec < rec_safe;
+    int wpb = 1, bps = 0;
+    if (int rc = size_launch(L.ring, rec, &L.warp_smem, &wpb, &bps)) return rc;
+    L.wpb = wpb;
+    L.blocks_per_sm = bps;
+    L.block = wpb * 32;
+    L.grid = h->sm_count * bps;
+    L.fb_wpb = L.wpb; L.fb_block = L.block; L.fb_grid = 0; L.fb_warp_smem = L.warp_smem;
+    if (L.fallback) {
+      int fw = 1, fb = 0;
+      if (int rc = size_launch(L.ring, rec_safe, &L.fb_warp_smem, &fw, &fb)) return rc;
+      L.fb_wpb = fw;
+      L.fb_block = fw * 32;
+      L.fb_grid = h->sm_count * fb;
+    }
+    return 0;
+  };
+  // member engine (every policy; explicit traces)
+  h->mem = LaunchCfg{};
+  h->mem.Rc_safe = derive_rc(h);
+  h->mem.Rc = speculative_rc(h, h->mem.Rc_safe);
+  if (int rc = size_cfg(h->mem)) return rc;
+  // class-ring engine: WAIT / FCFS with fixed per-class lengths
+  h->use_ring = false;
+  const char* eng = getenv("WAITSIM_ENGINE");
+  bool fixed = true;
+  for (int c = 0; c < K; ++c) fixed = fixed && h->in.l[c].size() == 1 && h->in.lp[c].size() == 1;
+  if (h->in.policy != SCHED_NESTED && fixed && !(eng && std::string(eng) == "member")) {
+    LaunchCfg& L = h->rng;
+    L = LaunchCfg{};
+    L.ring = true;
+    const auto& in = h->in;
+    uint64_t safe_tot = 0;
+    for (int c = 0; c < K; ++c) {
+      const uint32_t l = (uint32_t)in.l[c][0].first, lp = (uint32_t)in.lp[c][0].first;
+      uint64_t cs;
+      if (h->max_resident_cfg) cs = h->max_resident_cfg;
+      else if (in.policy == SCHED_WAIT) cs = (uint64_t)in.thresholds[c] * lp;  // P14: <= n_c per stage
+      else cs = std::min<uint64_t>(in.B, (uint64_t)in.M / l);
+      L.rcap_safe[c] = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(cs, 8192));
+      safe_tot += L.rcap_safe[c];
+    }
+    if (in.policy == SCHED_WAIT) {
+      uint64_t st = 0;
+      for (int c = 0; c < K; ++c) st += in.thresholds[c];
+      L.Rc_safe = (uint32_t)std::min<uint64_t>(st, 8192);
+    } else {
+      L.Rc_safe = h->max_resident_cfg ? h->max_resident_cfg : in.B;
+    }
+    L.Rc_safe = std::max<uint32_t>(L.Rc_safe, 1);
+    // speculative capacities: FCFS residents ~ fluid prompts in service n*_c
+    // + margin, staging ~ fluid admissions per batch + margin
+    L.Rc = L.Rc_safe;
+    for (int c = 0; c < K; ++c) L.rcap[c] = L.rcap_safe[c];
+    if (h->spec_resident_cfg) {
+      for (int c = 0; c < K; ++c)
+        L.rcap[c] = std::max<uint32_t>(1, std::min<uint32_t>(L.rcap_safe[c],
+                       (uint32_t)((uint64_t)h->spec_resident_cfg * L.rcap_safe[c] / std::max<uint64_t>(1, safe_tot))));
+      L.Rc = std::min<uint32_t>(L.Rc_safe, std::max<uint32_t>(32, h->spec_resident_cfg / 4));
+    } else if (is_fcfs(in.policy) && !h->max_resident_cfg && h->n_star_total > 0) {
+      // FCFS residents ~ fluid prompts in service n*_c, scaled
+      // by M / M* when memory binds and by B / n* when the batch cap binds
+      // (WAIT needs no speculation: n_c per stage exactly, P14)
+      const double fm = h->m_star > 0 ? std::min(1.0, (double)in.M / h->m_star) : 1.0;
+      const double tot = std::min((double)in.B, fm * h->n_star_total);
+      double adm = 0;
+      for (int c = 0; c < K; ++c) {
+        const double share = h->n_star_c[c] / h->n_star_total;
+        L.rcap[c] = std::min<uint32_t>(L.rcap_safe[c], (uint32_t)(1.2 * tot * share) + 48);
+        adm += h->n_star_c[c] / (double)(in.lp[c][0].first + 1);
+      }
+      L.Rc = std::min<uint32_t>(L.Rc_safe, round32((uint64_t)(1.5 * adm) + 64));
+    }
+    if (int rc = size_cfg(L)) return rc;
+    h->use_ring = true;
   }
   const int n_rings = h->in.policy == SCHED_WAIT ? K : 1;
-  const size_t slots = (size_t)std::max(h->grid * h->wpb, h->fb_grid * h->fb_wpb);
+  size_t slots = (size_t)std::max(h->mem.grid * h->mem.wpb, h->mem.fb_grid * h->mem.fb_wpb);
+  if (h->use_ring)
+    slots = std::max(slots, (size_t)std::max(h->rng.grid * h->rng.wpb, h->rng.fb_grid * h->rng.fb_wpb));
   const size_t need = slots * n_rings * h->ring_cap;
   if (need > h->ring_entries) {
     cudaFree(h->d_ring_a); cudaFree(h->d_ring_e); cudaFree(h->d_ring_llp);
@@ -230,10 +312,10 @@ int prepare(sched_s* h) {
   if (!h->d_counter) CK(cudaMalloc(&h->d_counter, 16));  // [main, fallback, retry count]
   DevParams& p = h->base;
   p.n_rings = n_rings;
-  p.Rc = h->Rc;
   p.ring_cap = h->ring_cap;
-  p.warp_smem = h->warp_smem;
   for (size_t i = 0; i < h->in.thresholds.size() && i < 32; ++i) p.thr[i] = h->in.thresholds[i];
+  for (int c = 0; c < K; ++c)
+    p.fl[c] = (uint32_t)h->in.l[c][0].first | ((uint32_t)h->in.lp[c].back().first << 16);
   p.ring_a = h->d_ring_a;
   p.ring_e = h->d_ring_e;
   p.ring_llp = h->d_ring_llp;
@@ -242,13 +324,27 @@ int prepare(sched_s* h) {
   return 0;
 }
 
-int launch(sched_s* h, DevParams p, cudaStream_t st) {
+// capacities of one launch of configuration L (safe = the fallback launch)
+void set_caps(DevParams& p, const LaunchCfg& L, bool safe, int K) {
+  p.ring_engine = L.ring ? 1u : 0u;
+  p.Rc = safe ? L.Rc_safe : L.Rc;
+  p.warp_smem = safe ? L.fb_warp_smem : L.warp_smem;
+  uint32_t off = 0;
+  for (int c = 0; c < K; ++c) {
+    p.rcap[c] = L.ring ? (safe ? L.rcap_safe[c] : L.rcap[c]) : 0u;
+    p.roff[c] = off;
+    off += p.rcap[c];
+  }
+}
+
+int launch(sched_s* h, DevParams p, cudaStream_t st, const LaunchCfg& L) {
+  const int K = p.K;
   CK(cudaMemsetAsync(h->d_counter, 0, 16, st));
   p.work_counter = h->d_counter;
   p.retry_count = h->d_counter + 2;
   p.retry_list = nullptr;
   p.fallback = 0;
-  if (h->fallback) {
+  if (L.fallback) {
     if (p.n_reps > h->retry_cap) {
       cudaFree(h->d_retry);
       h->d_retry = nullptr;
@@ -257,20 +353,20 @@ int launch(sched_s* h, DevParams p, cudaStream_t st) {
     }
     p.retry_list = h->d_retry;
   }
-  const size_t smem = (size_t)h->wpb * h->warp_smem;
-  int grid = h->grid;
-  const int warps = grid * h->wpb;
-  if ((int64_t)p.n_reps < warps) grid = std::max<int>(1, (int)((p.n_reps + h->wpb - 1) / h->wpb));
-  CK(launch_sim(p, grid, h->block, smem, st));
-  if (h->fallback) {
+  set_caps(p, L, false, K);
+  const size_t smem = (size_t)L.wpb * L.warp_smem;
+  int grid = L.grid;
+  const int warps = grid * L.wpb;
+  if ((int64_t)p.n_reps < warps) grid = std::max<int>(1, (int)((p.n_reps + L.wpb - 1) / L.wpb));
+  CK(launch_sim(p, grid, L.block, smem, st));
+  if (L.fallback) {
     // replications that overflowed the speculative capacity, re-run safely
     DevParams q = p;
     q.fallback = 1;
     q.work_counter = h->d_counter + 1;
-    q.Rc = h->Rc_safe;
-    q.warp_smem = h->fb_warp_smem;
-    const int fgrid = std::min(h->fb_grid, std::max(1, (int)((p.n_reps + h->fb_wpb - 1) / h->fb_wpb)));
-    CK(launch_sim(q, fgrid, h->fb_block, (size_t)h->fb_wpb * h->fb_warp_smem, st));
+    set_caps(q, L, true, K);
+    const int fgrid = std::min(L.fb_grid, std::max(1, (int)((p.n_reps + L.fb_wpb - 1) / L.fb_wpb)));
+    CK(launch_sim(q, fgrid, L.fb_block, (size_t)L.fb_wpb * L.fb_warp_smem, st));
   }
   return 0;
 }
@@ -483,7 +579,7 @@ int sched_run(sched_t h, uint64_t seed, uint64_t rep_begin, uint32_t n_reps, dou
   p.T_t = std::llround(horizon_s * 1e12);
   p.trace_mode = 0;
   p.out = out_dev;
-  return launch(h, p, (cudaStream_t)cuda_stream);
+  return launch(h, p, (cudaStream_t)cuda_stream, h->use_ring ? h->rng : h->mem);
 }
 
 int sched_run_host(sched_t h, uint64_t seed, uint64_t rep_begin, uint32_t n_reps,
@@ -562,7 +658,7 @@ int sched_run_trace(sched_t h, const int64_t* t_ticks, const int32_t* cls, const
     p.log = d_log;
     p.log_cap = log_host ? log_cap : 0;
     p.log_n = d_logn;
-    rc = launch(h, p, 0);
+    rc = launch(h, p, 0, h->mem);
     if (rc == 0) {
       e = cudaDeviceSynchronize();
       if (e == cudaSuccess) e = cudaMemcpy(out_host, d_out, out_bytes, cudaMemcpyDeviceToHost);
@@ -584,17 +680,23 @@ int sched_run_trace(sched_t h, const int64_t* t_ticks, const int32_t* cls, const
 int sched_get_launch_info(sched_t h, sched_launch_info* out) {
   if (!h || !out) return fail(SCHED_E_INVALID, "null argument");
   if (int rc = prepare(h)) return rc;
-  out->grid = h->grid;
-  out->block = h->block;
-  out->warps_per_block = h->wpb;
-  out->shared_bytes = (int32_t)(h->wpb * h->warp_smem);
-  out->blocks_per_sm = h->blocks_per_sm;
+  // the configuration sched_run uses (class-ring engine when eligible);
+  // capacities in resident records (ring engine: rings + staging slots)
+  const LaunchCfg& L = h->use_ring ? h->rng : h->mem;
+  uint32_t spec = L.Rc, safe = L.Rc_safe;
+  for (int c = 0; L.ring && c < (int)h->in.lambda.size(); ++c) { spec += L.rcap[c]; safe += L.rcap_safe[c]; }
+  out->grid = L.grid;
+  out->block = L.block;
+  out->warps_per_block = L.wpb;
+  out->shared_bytes = (int32_t)(L.wpb * L.warp_smem);
+  out->blocks_per_sm = L.blocks_per_sm;
   out->sm_count = h->sm_count;
-  out->max_resident = (int32_t)h->Rc_safe;
+  out->max_resident = (int32_t)safe;
   out->restart_cap = (int32_t)h->ring_cap;
-  out->spec_resident = (int32_t)h->Rc;
-  out->fallback_grid = h->fallback ? h->fb_grid : 0;
-  out->fallback_warps_per_block = h->fallback ? h->fb_wpb : 0;
+  out->spec_resident = (int32_t)spec;
+  out->fallback_grid = L.fallback ? L.fb_grid : 0;
+  out->fallback_warps_per_block = L.fallback ? L.fb_wpb : 0;
+  out->engine = L.ring ? 1 : 0;
   return SCHED_OK;
 }
 

@@ -25,7 +25,15 @@ struct DevParams {
   int64_t d0_t, d1_t, T_t, M;
   uint32_t thr[kMaxSegments];      // WAIT: per class, NESTED: per segment
   uint32_t B, tok_budget;
-  uint32_t Rc;             // resident capacity per replication
+  uint32_t Rc;             // resident capacity per replication (class-ring engine: staging capacity)
+  // class-ring engine: fixed-length classes under WAIT /
+  // FCFS keep their residents in per-class rings in admission order; stage
+  // = class clock - admission clock, so a batch touches only the members
+  // that complete, emit a first token or are admitted
+  uint32_t ring_engine;
+  uint32_t rcap[kMaxClasses];      // ring capacity (records) of class c
+  uint32_t roff[kMaxClasses];      // first record of ring c after the staging area
+  uint32_t fl[kMaxClasses];        // fixed l | l' << 16 of class c
   uint32_t ring_cap;       // restart ring capacity (entries) per ring
   uint32_t warp_smem;      // bytes of shared memory per warp
   uint64_t seed;
@@ -67,18 +75,19 @@ struct DevParams {
 };
 
 // shared-memory bytes per warp for a given resident capacity / class count
-inline uint32_t warp_smem_bytes(uint32_t Rc, int K, bool tv = false) {
+inline uint32_t warp_smem_bytes(uint32_t Rc, int K, bool tv = false, bool ring = false) {
   uint32_t b = Rc * 16u;                    // residents: a (i64) + packed (l, l', s, meta)
   b += (uint32_t)K * (32u * 12u);           // generated windows (t, l, l')
   b += (uint32_t)K * (32u * 12u);           // private admission windows (t, l, l')
   b += 32u * 8u;                            // staged restart ticks
   b += (64u + 32u + 32u) * 4u + 16u;        // counters, rank cursors, snapshot, align
   b += 256u;                                // WarpStats (metric accumulators)
+  if (ring) b += 256u;                      // class-ring eviction scratch
   if (tv) b += (uint32_t)K * (32u * 16u);   // operational-time windows (generated, private)
   return (b + 15u) & ~15u;
 }
 
 cudaError_t launch_sim(const DevParams& p, int grid, int block, size_t smem, cudaStream_t s);
-cudaError_t sim_occupancy(int policy, int trace, int block, size_t smem, int* blocks_per_sm);
+cudaError_t sim_occupancy(int policy, int trace, int block, size_t smem, int* blocks_per_sm, int ring = 0);
 
 }  // namespace waitsim

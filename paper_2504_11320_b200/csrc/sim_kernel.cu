@@ -125,6 +125,14 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
 }
+// shared-memory reductions (explicit .shared: the generic atomics the
+// compiler emits for smem pointers it cannot prove are slower)
+__device__ __forceinline__ void sh_add_u32(uint32_t* p, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sh_add_u64(uint64_t* p, uint64_t v) {
+  asm volatile("red.shared.add.u64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "l"(v) : "memory");
+}
 __device__ __forceinline__ int64_t bcast64(int64_t v, int src) { return __shfl_sync(FULL, v, src); }
 __device__ __forceinline__ uint32_t bcast32(uint32_t v, int src) { return __shfl_sync(FULL, v, src); }
 
@@ -138,7 +146,18 @@ constexpr uint32_t META_RESTART = 0x200;
 struct __align__(16) Rec {
   int64_t a;
   uint64_t q;
-};  // staging mark: came from a restart ring
+};
+// class-ring engine resident: arrival tick, admission clock x (bits 0-29) |
+// first token pending at the next participation (bit 30, valid while
+// x = C - 1) | first token emitted or pending (bit 31), admission sequence
+// number (LIFO order)
+struct __align__(16) RRec {
+  int64_t a;
+  uint32_t xf;
+  uint32_t seq;
+};
+constexpr uint32_t XF_FT = 0x80000000u, XF_PEND = 0x40000000u, XF_X = 0x3FFFFFFFu;
+__device__ __forceinline__ uint32_t wrap(uint32_t p, uint32_t cap) { return p >= cap ? p - cap : p; }  // staging mark: came from a restart ring
 
 // # of leading entries of the sorted array v[0..n) that precede `key`
 // (v <= key if le, v < key otherwise)
@@ -236,12 +255,13 @@ __device__ __forceinline__ void gen_window(GEN_WINDOW_ARGS) {
   else gen_window_call(GEN_WINDOW_PASS);
 }
 
-template <int POL, bool TRACE>
+template <int POL, bool TRACE, bool RING>
 struct WarpSim {
   const DevParams& P;
   const int lane;
   // shared-memory views (this warp's slice)
-  Rec* rr;                           // [Rc] residents in admission order
+  Rec* rr;                           // [Rc] residents in admission order (RING: staged admissions)
+  RRec* rg;                          // RING: class rings (ring c at P.roff[c], P.rcap[c] records)
   int64_t* vt;                       // [K][32] generated window (t): visibility + admission
   uint16_t* vl; uint16_t* vlp;       // [K][32] generated window (l, l')
   int64_t* at;                       // [K][32] private admission windows (t)
@@ -252,6 +272,7 @@ struct WarpSim {
   uint32_t* rank;                    // [32] NESTED per-segment rank cursors
   uint32_t* snap;                    // [32] NESTED entry counts at decision time
   WarpStats* st;                     // metric accumulators
+  uint64_t* xs;                      // [32] RING eviction scratch (per-class sums)
   size_t ring_base;                  // first ring entry of this warp slot
 
   // per-class cursor state, lane c holds class c (and ring c for WAIT; ring 0
@@ -266,6 +287,14 @@ struct WarpSim {
   uint32_t sv_k, sv_rhead;           // saved admission cursor (drop/rewind)
   int64_t sv_prev;
   uint32_t newc;                     // WAIT: admissions of class `lane` this epoch
+
+  // RING: lane c holds class c's ring (head position, residents, clock =
+  // batches class c took part in, sum of admission clocks) + next sequence no.
+  uint32_t r_head, r_n, r_C, seq_next;
+  uint64_t r_X;
+  // RING: first tokens pending at class c's next participation: count in
+  // cnt[32 + c], arrival-tick sum in psum()[c] (the NESTED rank / snap slots)
+  __device__ __forceinline__ uint64_t* psum() const { return (uint64_t*)rank; }
 
   // replication
   uint32_t rep, rglob;
@@ -283,18 +312,23 @@ struct WarpSim {
       : P(p), lane(lane_), ring_base(rb) {
     const uint32_t Rc = p.Rc;
     rr = (Rec*)base;
-    vt = (int64_t*)(rr + Rc);
+    // RING: 32 spare staging slots hold the victims of one eviction round
+    rg = (RRec*)(rr + Rc + (RING ? 32u : 0u));
+    vt = (int64_t*)(rr + Rc + (RING ? 32u + p.roff[p.K - 1] + p.rcap[p.K - 1] : 0u));
     at = vt + p.K * 32;
     re = at + p.K * 32;
-    al = (uint16_t*)(re + 32);
-    alp = al + p.K * 32;
-    vl = alp + p.K * 32;
-    vlp = vl + p.K * 32;
-    cnt = (uint32_t*)(((uintptr_t)(vlp + p.K * 32) + 15) & ~(uintptr_t)15);
+    // l / l' of both windows share one offset space with the ticks:
+    // offset o < 32K is vt[o] / vl[o] / vlp[o], 32K <= o < 64K the private window
+    vl = (uint16_t*)(re + 32);
+    al = vl + p.K * 32;
+    vlp = al + p.K * 32;
+    alp = vlp + p.K * 32;
+    cnt = (uint32_t*)(((uintptr_t)(alp + p.K * 32) + 15) & ~(uintptr_t)15);
     rank = cnt + 64;
     snap = rank + 32;
     st = (WarpStats*)(snap + 32);
-    vtau = (int64_t*)((unsigned char*)st + 256);
+    xs = (uint64_t*)((unsigned char*)st + 256);
+    vtau = (int64_t*)((unsigned char*)st + (RING ? 512 : 256));
     atau = vtau + p.K * 32;
   }
 
@@ -440,6 +474,9 @@ struct WarpSim {
   // number of candidates before it (binary searches over the other sources'
   // windows); FCFS additionally cuts at the first prompt failing the
   // admission test (reading R15).
+  // first staging slot: after the residents (member engine) or 0 (RING)
+  __device__ __forceinline__ uint32_t sbase() const { return RING ? 0u : n_res; }
+
   // FCFS admission cut: lane i holds staged candidate i (prefill length l);
   // the longest prefix passing the test of PAPER.md:1427, 1745 (R15)
   __device__ __forceinline__ uint32_t fcfs_take(uint32_t m, uint32_t l) const {
@@ -454,19 +491,40 @@ struct WarpSim {
   }
 
   // take_fifo fast path, one source class c (WAIT, or a single class): the
-  // FIFO head is arrivals k_adm .. of class c, read in order from its window
+  // FIFO head is arrivals k_adm .. of class c, read in order from its
+  // windows.  Returns -1 capacity error, 0 done, 1 took a full chunk.
+  // the first (<= 32) waiting arrivals of a class: window offsets o1 ..
+  // o1+len1-1, then o2 ..
+  struct Seg {
+    uint32_t o1, len1, o2;
+    __device__ __forceinline__ uint32_t at(uint32_t i) const { return i < len1 ? o1 + i : o2 + (i - len1); }
+    __device__ __forceinline__ Seg from(int c) const {
+      return Seg{__shfl_sync(FULL, o1, c), __shfl_sync(FULL, len1, c), __shfl_sync(FULL, o2, c)};
+    }
+  };
+  // # of the first n candidates of segment sg with tick <= key (le) or < key
+  __device__ __forceinline__ uint32_t count_before_seg(const Seg& sg, uint32_t n, int64_t key, bool le) const {
+    uint32_t lo = 0, len = n;
+    while (len > 0) {
+      const uint32_t half = len >> 1;
+      const int64_t x = vt[sg.at(lo + half)];
+      if (le ? (x <= key) : (x < key)) { lo += half + 1; len -= half + 1; } else { len = half; }
+    }
+    return lo;
+  }
+
   template <bool FCFS_COND>
-  __device__ __forceinline__ bool take_single(int c, uint32_t pend, uint32_t& want) {
+  __device__ __forceinline__ int take_single(int c, uint32_t pend, const Seg& sgl, uint32_t& want) {
     const uint32_t p = bcast32(pend, c);
-    const uint32_t o = bcast32(k_adm - vbase, c);  // unused if p == 0
-    const uint32_t base = n_res + n_new;
+    const Seg sg = sgl.from(c);
+    const uint32_t base = sbase() + n_new;
     uint32_t m = min(p, want);
     if (FCFS_COND) m = min(m, P.B > base ? P.B - base : 0u);
-    if (m == 0) return true;
-    if (base + m > P.Rc) { status = 1; return false; }
+    if (m == 0) return 0;
+    if (base + m > P.Rc) { status = 1; return -1; }
     uint32_t l = 0;
     if ((uint32_t)lane < m) {
-      const int idx = c * 32 + (int)(o + lane);
+      const uint32_t idx = sg.at((uint32_t)lane);
       l = vl[idx];
       rr[base + lane] = Rec{vt[idx], pack_q(l, vlp[idx], 1, (uint32_t)c)};
     }
@@ -476,7 +534,7 @@ struct WarpSim {
     sum_new_l += __reduce_add_sync(FULL, (uint32_t)lane < take ? l : 0u);
     want -= take;
     __syncwarp();
-    return true;
+    return take < m ? 0 : 1;
   }
 
   // take_fifo fast path, several classes merged by (t, class): candidate g
@@ -484,12 +542,11 @@ struct WarpSim {
   // binary search over their windows.  Returns -1 capacity error, 0 done,
   // 1 took a full chunk (more may follow).
   template <bool FCFS_COND>
-  __device__ __forceinline__ int take_merged(uint32_t pend, uint32_t& want) {
-    const uint32_t my_o = pend ? k_adm - vbase : 0u;
+  __device__ __forceinline__ int take_merged(uint32_t pend, const Seg& my, uint32_t& want) {
     const uint32_t incl = warp_incl_scan_u32(pend, lane);  // lanes >= K: pend = 0
     const uint32_t ncand = __shfl_sync(FULL, incl, 31);
     if (ncand == 0) return 0;
-    const uint32_t base = n_res + n_new;
+    const uint32_t base = sbase() + n_new;
     uint32_t m = min(min(ncand, 32u), want);
     if (FCFS_COND) m = min(m, P.B > base ? P.B - base : 0u);
     if (m == 0) return 0;
@@ -501,15 +558,17 @@ struct WarpSim {
       int s = 0;  // source class: first class whose candidate range ends after g
       for (int c = 0; c < K; ++c) s += bcast32(incl, c) <= g;
       s = min(s, K - 1);
-      const uint32_t s_n = __shfl_sync(FULL, pend, s), s_o = __shfl_sync(FULL, my_o, s);
+      const uint32_t s_n = __shfl_sync(FULL, pend, s);
+      const Seg ss{__shfl_sync(FULL, my.o1, s), __shfl_sync(FULL, my.len1, s), __shfl_sync(FULL, my.o2, s)};
       const uint32_t pos = g - (__shfl_sync(FULL, incl, s) - s_n);
-      const int idx = s * 32 + (int)(s_o + pos);
+      const uint32_t idx = ss.at(pos);
       const int64_t t = act ? vt[idx] : 0;
       uint32_t r = pos;
       for (int c = 0; c < K; ++c) {
-        const uint32_t n = bcast32(pend, c), o = bcast32(my_o, c);
+        const uint32_t n = bcast32(pend, c);
+        const Seg sc = my.from(c);
         // ties: a lower class index precedes
-        if (act && c != s && n) r += count_before(vt + c * 32 + o, n, t, c < s);
+        if (act && c != s && n) r += count_before_seg(sc, n, t, c < s);
       }
       if (act && r < m) {
         rr[base + r] = Rec{t, pack_q(vl[idx], vlp[idx], 1, (uint32_t)s)};
@@ -545,13 +604,30 @@ struct WarpSim {
       {
         const bool in_rng = lane >= c_lo && lane < c_hi;
         const uint32_t pend = in_rng ? k_vis - k_adm : 0u;
-        const bool ok = (pend == 0 || k_adm >= vbase) && (lane != q || rtail == rhead);
-        if (__all_sync(FULL, ok)) {
-          if (c_hi - c_lo == 1) {
-            if (!take_single<FCFS_COND>(c_lo, pend, want)) return false;
-            break;
+        // class `lane`'s waiting arrivals as offsets: the generated window
+        // (attached) or the private window continuing into it
+        uint32_t o1 = 0, len1 = 32, o2 = 0;
+        bool ok = lane != q || rtail == rhead;
+        if (pend) {
+          if (k_adm >= vbase) {
+            o1 = lane * 32 + (k_adm - vbase);
+          } else if (k_adm >= abase && abase + pcount == vbase) {
+            o1 = (P.K + lane) * 32 + (k_adm - abase);
+            len1 = abase + pcount - k_adm;
+            o2 = lane * 32;
+          } else {
+            ok = false;
           }
-          const int r = take_merged<FCFS_COND>(pend, want);
+        }
+        if (__all_sync(FULL, ok)) {
+          const Seg sg{o1, len1, o2};
+          if (c_hi - c_lo == 1) {
+            const int r = take_single<FCFS_COND>(c_lo, min(pend, 32u), sg, want);
+            if (r < 0) return false;
+            if (r == 0) break;
+            continue;
+          }
+          const int r = take_merged<FCFS_COND>(min(pend, 32u), sg, want);
           if (r < 0) return false;
           if (r == 0) break;
           continue;
@@ -599,7 +675,7 @@ struct WarpSim {
       }
       const uint32_t ncand = total + nr;
       if (ncand == 0) break;
-      const uint32_t base = n_res + n_new;
+      const uint32_t base = sbase() + n_new;
       // stage at most what can be taken: `want` (WAIT/NESTED) or the B bound (FCFS)
       uint32_t m = min(min(ncand, 32u), want);
       if (FCFS_COND) m = min(m, P.B > base ? P.B - base : 0u);
@@ -737,7 +813,7 @@ struct WarpSim {
       uint32_t qq = 0, npr = 0;
       if (lane < P.K) {
         const uint32_t w = k_vis - k_adm + (rtail - rhead);
-        if (w >= P.thr[lane]) { qq = 1; npr = cnt[lane]; }
+        if (w >= P.thr[lane]) { qq = 1; npr = RING ? r_n : cnt[lane]; }
       }
       Qmask = __ballot_sync(FULL, qq);
       if (!Qmask) return false;
@@ -824,8 +900,8 @@ struct WarpSim {
         P.ring_a[e] = a;
         P.ring_e[e] = now;
         P.ring_llp[e] = l | (lp << 16) | ((meta & META_FT) ? 0x80000000u : 0u);
-        if (POL == SCHED_WAIT) atomicSub(&cnt[meta & 0xFF], 1u);
-        if (POL == SCHED_NESTED) atomicSub(&cnt[nkey], 1u);
+        if (POL == SCHED_WAIT) sh_add_u32(&cnt[meta & 0xFF], ~0u);
+        if (POL == SCHED_NESTED) sh_add_u32(&cnt[nkey], ~0u);
       }
       if (POL == SCHED_WAIT) {  // advance ring tails (lane q owns ring q)
         for (int c = 0; c < P.K; ++c) {
@@ -854,16 +930,123 @@ struct WarpSim {
         __syncwarp();
       }
     }
-    if (excess > 0) {
-      // no residents left: drop the latest new admissions (they stay queued)
-      uint32_t keep = n_new;
-      while (excess > 0 && keep > 0) { excess -= (int64_t)(rr[n_res + keep - 1].q & 0xFFFF); --keep; }
-      restore_cursors();
-      n_new = 0;
-      sum_new_l = 0;
-      if (POL == SCHED_WAIT) take_wait(keep);
-      else take_fifo<false>(0, keep);  // FCFS never gets here (admission bound)
+    if (excess > 0) drop_admissions(excess);
+    peak = P.M + excess;
+  }
+
+  // no residents left and still over M: drop the latest new admissions
+  // (they stay queued) and re-take the kept prefix in FIFO order
+  __device__ void drop_admissions(int64_t& excess) {
+    uint32_t keep = n_new;  // n_res == 0: staged admissions start at slot 0
+    while (excess > 0 && keep > 0) { excess -= (int64_t)(rr[keep - 1].q & 0xFFFF); --keep; }
+    restore_cursors();
+    n_new = 0;
+    sum_new_l = 0;
+    if (POL == SCHED_WAIT) take_wait(keep);
+    else take_fifo<false>(0, keep);  // FCFS never gets here (admission bound)
+  }
+
+  // S4 for the class-ring engine: LIFO eviction of up
+  // to 32 victims per round.  The newest residents are the class-ring tails;
+  // each tail record's LIFO rank = its depth in its own ring + the number of
+  // newer (larger sequence number) tail records of the other classes, by
+  // binary search; then an inclusive scan of freed KV finds the cut.
+  __device__ __forceinline__ uint32_t ring_tail_idx(uint32_t off, uint32_t head, uint32_t n, uint32_t cap,
+                                                    uint32_t j) const {
+    return off + wrap(head + (n - 1 - j), cap);  // j-th newest resident of a class
+  }
+  __device__ void memory_ring(uint32_t& n_evict, int64_t& peak) {
+    peak = KV + (int64_t)n_plan_res + sum_new_l;
+    if (peak <= P.M) return;
+    int64_t excess = peak - P.M;
+    const int K = P.K;
+    while (excess > 0 && n_res > 0) {
+      const uint32_t nc = lane < K ? min(r_n, 32u) : 0u;  // class `lane`'s tail window
+      const uint32_t incl = warp_incl_scan_u32(nc, lane);
+      const uint32_t ncand = __shfl_sync(FULL, incl, 31);
+      const uint32_t my_off = lane < K ? P.roff[lane] : 0u, my_cap = lane < K ? P.rcap[lane] : 1u;
+      // (1) rank every tail-window record; rank < 32 -> victim slot
+      for (uint32_t g0 = 0; g0 < ncand; g0 += 32) {
+        const uint32_t g = g0 + (uint32_t)lane;
+        const bool act = g < ncand;
+        int sc = 0;
+        for (int c = 0; c < K; ++c) sc += bcast32(incl, c) <= g;
+        sc = min(sc, K - 1);
+        const uint32_t j = g - (__shfl_sync(FULL, incl, sc) - __shfl_sync(FULL, nc, sc));
+        const uint32_t idx = ring_tail_idx(__shfl_sync(FULL, my_off, sc), __shfl_sync(FULL, r_head, sc),
+                                           __shfl_sync(FULL, r_n, sc), __shfl_sync(FULL, my_cap, sc), j);
+        RRec e = {0, 0, 0};
+        if (act) e = rg[idx];
+        uint32_t r = j;
+        for (int c = 0; c < K; ++c) {
+          const uint32_t n = bcast32(nc, c);
+          const uint32_t off = bcast32(my_off, c), head = bcast32(r_head, c), rn = bcast32(r_n, c),
+                         cap = bcast32(my_cap, c);  // (all lanes: shuffles before any divergence)
+          if (!act || c == sc || n == 0) continue;
+          uint32_t lo = 0, len = n;  // # of class-c tail records newer than e
+          while (len > 0) {
+            const uint32_t half = len >> 1;
+            if (rg[ring_tail_idx(off, head, rn, cap, lo + half)].seq > e.seq) { lo += half + 1; len -= half + 1; }
+            else len = half;
+          }
+          r += lo;
+        }
+        __syncwarp();
+        if (act && r < 32) { rr[sbase() + n_new + r] = Rec{e.a, (uint64_t)e.xf | ((uint64_t)sc << 32)}; }
+        __syncwarp();
+      }
+      // (2) victims in LIFO order: lane r holds the r-th newest resident
+      const uint32_t nv = min(ncand, 32u);
+      const bool valid = (uint32_t)lane < nv;
+      Rec e = {0, 0};
+      if (valid) e = rr[sbase() + n_new + lane];
+      const uint32_t xf = (uint32_t)e.q, v = (uint32_t)(e.q >> 32) & 31u;
+      const uint32_t x = xf & XF_X, Cv = __shfl_sync(FULL, r_C, (int)v);
+      const uint32_t fl = P.fl[v], l = fl & 0xFFFFu, lp = fl >> 16;
+      const uint32_t s = Cv - x;  // next stage to run
+      const uint32_t inp = valid && (POL == SCHED_WAIT ? ((Qmask >> v) & 1u) : 1u);
+      const uint32_t f = valid ? (l + s - 1 + inp) : 0u;
+      const uint32_t cum = warp_incl_scan_u32(f, lane);
+      const uint32_t hit = __ballot_sync(FULL, valid && (int64_t)cum >= excess);
+      const uint32_t ne = hit ? (uint32_t)__ffs(hit) : nv;
+      const bool ev = (uint32_t)lane < ne;
+      // a first token still pending (admitted at the last participation) was not emitted
+      const bool pend = ev && (xf & XF_PEND) && x == Cv - 1;
+      // restart records in eviction order (re-enter the queue)
+      const int q = POL == SCHED_WAIT ? (int)v : 0;
+      const uint32_t grp = __match_any_sync(FULL, ev ? (uint32_t)q : (0x100u + (uint32_t)lane));
+      const uint32_t before = __popc(grp & lanemask_lt());
+      const uint32_t tail_q = __shfl_sync(FULL, rtail, q), head_q = __shfl_sync(FULL, rhead, q);
+      if (__any_sync(FULL, ev && (tail_q - head_q + before + 1 > P.ring_cap))) { status = 2; return; }
+      cnt[lane] = 0;
+      xs[lane] = 0;
+      __syncwarp();
+      if (ev) {
+        const size_t ri = ring_slot(q, tail_q + before);
+        P.ring_a[ri] = e.a;
+        P.ring_e[ri] = now;
+        P.ring_llp[ri] = l | (lp << 16) | (((xf & XF_FT) && !pend) ? 0x80000000u : 0u);
+        sh_add_u32(&cnt[v], 1u);
+        sh_add_u64(&xs[v], (uint64_t)x);
+        if (pend) { sh_add_u32(&cnt[32 + v], ~0u); sh_add_u64(&psum()[v], (uint64_t)(-e.a)); }
+      }
+      __syncwarp();
+      if (lane < K) {
+        const uint32_t k = cnt[lane];
+        r_n -= k;
+        r_X -= xs[lane];
+        if (POL == SCHED_WAIT) rtail += k;  // ring q = class q
+      }
+      if (POL != SCHED_WAIT && lane == 0) rtail += ne;
+      if (lane == 0) st->evictions += ne;
+      excess -= (int64_t)__reduce_add_sync(FULL, ev ? f : 0u);
+      KV -= (int64_t)__reduce_add_sync(FULL, ev ? (l + s - 1) : 0u);
+      n_plan_res -= __reduce_add_sync(FULL, ev ? inp : 0u);
+      n_res -= ne;
+      n_evict += ne;
+      __syncwarp();
     }
+    if (excess > 0) drop_admissions(excess);
     peak = P.M + excess;
   }
 
@@ -923,8 +1106,8 @@ struct WarpSim {
         ++acc.n_done;
         acc.done_tok += u.lp;
         acc.done_a += (uint64_t)a;
-        if (POL == SCHED_WAIT) atomicSub(&cnt[u.meta & 0xFF], 1u);
-        if (POL == SCHED_NESTED) atomicSub(&cnt[key_s], 1u);
+        if (POL == SCHED_WAIT) sh_add_u32(&cnt[u.meta & 0xFF], ~0u);
+        if (POL == SCHED_NESTED) sh_add_u32(&cnt[key_s], ~0u);
       } else {
         u.ns = s + 1;
         ++acc.grow;
@@ -933,8 +1116,8 @@ struct WarpSim {
           // (-> the next segment's entry stage)
           const uint32_t seg = info_seg(info_s);
           const uint32_t key_n = (info_s & 0x40) ? 32u + seg + 1u : seg;
-          atomicSub(&cnt[key_s], 1u);
-          atomicAdd(&cnt[key_n], 1u);
+          sh_add_u32(&cnt[key_s], ~0u);
+          sh_add_u32(&cnt[key_n], 1u);
         }
       }
     }
@@ -971,7 +1154,7 @@ struct WarpSim {
     acc.kv_free += done ? l + lp - 1 : 0u;
     acc.done_a += done ? (uint64_t)e.a : 0ull;
     acc.grow += inp && !done;
-    if (POL == SCHED_WAIT && done) atomicSub(&cnt[meta & 0xFF], 1u);
+    if (POL == SCHED_WAIT && done) sh_add_u32(&cnt[meta & 0xFF], ~0u);
     const uint64_t nq = q + ((inp && !done) ? (1ull << 32) : 0ull) + (ft ? ((uint64_t)META_FT << 48) : 0ull);
     const bool keep = v && !done;
     const uint32_t km = __ballot_sync(FULL, keep);
@@ -984,6 +1167,118 @@ struct WarpSim {
   // One pass over residents (+ the staged admissions) in admission order:
   // per-member update, completions, compaction; counters updated in place.
   __device__ void execute(uint32_t n_evict, int64_t peak, uint32_t waiting) {
+    uint32_t tok, nd, nf, dtok, kvf, gr;
+    uint64_t done_a = 0, ft_a = 0;
+    if (RING) {
+      ring_pass(tok, nd, nf, dtok, kvf, done_a, ft_a);
+      gr = n_plan_res - nd;
+      if (!ring_append()) return;
+      if (lane < P.K && (POL == SCHED_WAIT ? ((Qmask >> lane) & 1u) : 1u)) ++r_C;
+      n_res = n_res - nd + n_new;
+    } else {
+      member_pass(tok, nd, nf, dtok, kvf, gr, done_a, ft_a);
+    }
+    epilogue(n_evict, peak, waiting, tok, nd, nf, dtok, kvf, gr, done_a, ft_a);
+  }
+
+  // S5 for the class-ring engine: the stage of a member admitted at class
+  // clock x is C_c - x, so the stage-l' completions are a prefix of ring c
+  // and the stage-1 first tokens are
+  // the prompts admitted at the class's previous participation without one
+  // (counted at append); plan tokens sum_(l + s) = n_c (l_c + C_c) - sum x
+  __device__ void ring_pass(uint32_t& tok, uint32_t& nd, uint32_t& nf, uint32_t& dtok, uint32_t& kvf,
+                            uint64_t& done_a, uint64_t& ft_a) {
+    const bool cin = lane < P.K && (POL == SCHED_WAIT ? ((Qmask >> lane) & 1u) : 1u);
+    const uint32_t fl = lane < P.K ? P.fl[lane] : 0u, l = fl & 0xFFFFu, lp = fl >> 16;
+    const uint32_t tk = cin ? (uint32_t)((uint64_t)r_n * (l + r_C) - r_X) : 0u;
+    uint32_t my_nd = 0, my_nf = 0;
+    if (cin) {  // stage-1 members emit their first token
+      my_nf = cnt[32 + lane];
+      ft_a += psum()[lane];
+      cnt[32 + lane] = 0;
+      psum()[lane] = 0;
+    }
+    uint32_t cm = __ballot_sync(FULL, cin && r_n > 0);
+    while (cm) {
+      const int c = __ffs(cm) - 1;
+      cm &= cm - 1;
+      const uint32_t n = bcast32(r_n, c), head = bcast32(r_head, c), C = bcast32(r_C, c);
+      const uint32_t cap = P.rcap[c], lpc = P.fl[c] >> 16;
+      const RRec* R = rg + P.roff[c];
+      // completions: stage-l' members (x = C - l') from the head
+      uint32_t ndc = 0;
+      if (C >= lpc) {
+        for (uint32_t j0 = 0; j0 < n; j0 += 32) {
+          const uint32_t j = j0 + (uint32_t)lane;
+          bool dn = false;
+          if (j < n) {
+            const RRec* e = R + wrap(head + j, cap);
+            dn = (e->xf & XF_X) == C - lpc;
+            if (dn) done_a += (uint64_t)e->a;
+          }
+          const uint32_t m = __ballot_sync(FULL, dn);
+          ndc += __popc(m);
+          if (m != FULL) break;
+        }
+      }
+      if (lane == c) {
+        my_nd = ndc;
+        r_head = wrap(r_head + ndc, cap);
+        r_n -= ndc;
+        r_X -= (uint64_t)ndc * (C - lpc);
+      }
+    }
+    tok = __reduce_add_sync(FULL, tk);
+    nd = __reduce_add_sync(FULL, my_nd);
+    nf = __reduce_add_sync(FULL, my_nf);
+    dtok = __reduce_add_sync(FULL, my_nd * lp);
+    kvf = __reduce_add_sync(FULL, my_nd * (l + lp - 1));
+    __syncwarp();
+  }
+
+  // append the staged admissions (stage 1 next, admission clock = C_c) to
+  // their class rings, in admission order; false on ring overflow (status 1:
+  // the replication is re-run with the safe capacity)
+  __device__ bool ring_append() {
+    for (uint32_t j0 = 0; j0 < n_new; j0 += 32) {
+      const uint32_t j = j0 + (uint32_t)lane;
+      const bool v = j < n_new;
+      Rec e = {0, 0};
+      if (v) e = rr[j];
+      const uint32_t meta = (uint32_t)(e.q >> 48), c = v ? (meta & 0xFFu) : 0u;
+      const uint32_t grp = __match_any_sync(FULL, v ? c : 0x100u + (uint32_t)lane);
+      const uint32_t rk = __popc(grp & lanemask_lt());
+      const uint32_t n = __shfl_sync(FULL, r_n, (int)c), head = __shfl_sync(FULL, r_head, (int)c);
+      const uint32_t C = __shfl_sync(FULL, r_C, (int)c), cap = P.rcap[c];
+      if (__any_sync(FULL, v && n + rk >= cap)) { status = 1; return false; }
+      cnt[lane] = 0;
+      __syncwarp();
+      // a prompt without its first token emits it at the next participation
+      const bool pend = v && !(meta & META_FT);
+      if (v) {
+        rg[P.roff[c] + wrap(head + n + rk, cap)] = RRec{e.a, C | XF_FT | (pend ? XF_PEND : 0u), seq_next + j};
+        if (rk == 0) cnt[c] = __popc(grp);
+      }
+      if (pend) {  // per-class pending first tokens (shared: pcnt = cnt[32..], psum)
+        sh_add_u32(&cnt[32 + c], 1u);
+        sh_add_u64(&psum()[c], (uint64_t)e.a);
+      }
+      __syncwarp();
+      if (lane < P.K) {
+        const uint32_t k = cnt[lane];
+        r_n += k;
+        r_X += (uint64_t)k * r_C;
+      }
+      __syncwarp();
+    }
+    seq_next += n_new;
+    return true;
+  }
+
+  // S5 for the member engine: one pass over residents (+ the staged
+  // admissions) in admission order, per-member update and compaction
+  __device__ void member_pass(uint32_t& tok_o, uint32_t& nd_o, uint32_t& nf_o, uint32_t& dtok_o,
+                              uint32_t& kvf_o, uint32_t& gr_o, uint64_t& done_a_o, uint64_t& ft_a_o) {
     const uint32_t n_tot = n_res + n_new;
     uint32_t over = 0;  // NESTED: active segments whose entry queue exceeds n_k
     if (POL == SCHED_NESTED) {
@@ -1019,18 +1314,24 @@ struct WarpSim {
       }
     }
     __syncwarp();
-    uint32_t tok = acc.tok, n_done = acc.n_done, done_tok = acc.done_tok, n_ft = acc.n_ft,
-             kv_free = acc.kv_free, grow = acc.grow;
-    const uint64_t done_a = acc.done_a, ft_a = acc.ft_a;
     if (POL == SCHED_WAIT) { if (lane < P.K) cnt[lane] += newc; }
     if (POL == SCHED_NESTED) { if (lane == 0) cnt[0] += n_new; }  // stage 1 = segment 1, non-entry
     // warp-uniform batch totals
-    tok = __reduce_add_sync(FULL, tok);
-    const uint32_t nd = __reduce_add_sync(FULL, n_done);
-    const uint32_t nf = __reduce_add_sync(FULL, n_ft);
-    const uint32_t dtok = __reduce_add_sync(FULL, done_tok);
-    const uint32_t kvf = __reduce_add_sync(FULL, kv_free);
-    const uint32_t gr = __reduce_add_sync(FULL, grow);
+    tok_o = __reduce_add_sync(FULL, acc.tok);
+    nd_o = __reduce_add_sync(FULL, acc.n_done);
+    nf_o = __reduce_add_sync(FULL, acc.n_ft);
+    dtok_o = __reduce_add_sync(FULL, acc.done_tok);
+    kvf_o = __reduce_add_sync(FULL, acc.kv_free);
+    gr_o = __reduce_add_sync(FULL, acc.grow);
+    done_a_o = acc.done_a;
+    ft_a_o = acc.ft_a;
+    n_res = wp;
+  }
+
+  // batch epilogue: tau, clock, KV, metric accumulators, trajectory hash
+  __device__ void epilogue(uint32_t n_evict, int64_t peak, uint32_t waiting, uint32_t tok, uint32_t nd,
+                           uint32_t nf, uint32_t dtok, uint32_t kvf, uint32_t gr, uint64_t done_a,
+                           uint64_t ft_a) {
     const int64_t tokens = (int64_t)tok + sum_new_l;
     // tau = d0 + d1 * (sum prefill l + sum decode (l+s))
     const int64_t tau = P.d0_t + P.d1_t * tokens;
@@ -1070,7 +1371,6 @@ struct WarpSim {
       ++st->batches;
     }
     maybe_flush();
-    n_res = wp;
     n_new = 0;
     now = t_end;
     __syncwarp();
@@ -1093,6 +1393,9 @@ struct WarpSim {
     k_vis = vbase = k_adm = abase = pcount = rhead = rtail = 0;
     vprev = aprev = 0;
     newc = 0;
+    r_head = r_n = r_C = seq_next = 0;
+    r_X = 0;
+    if (RING) psum()[lane] = 0;
     for (int c = 0; c < P.K; ++c) {
       fill<true>(c, 0, 0, vt, vl, vlp);
     }
@@ -1108,7 +1411,8 @@ struct WarpSim {
       uint32_t n_evict = 0;
       int64_t peak = 0;
       if (go) {
-        memory(n_evict, peak);
+        if (RING) memory_ring(n_evict, peak);
+        else memory(n_evict, peak);
         if (status) break;
         if (n_plan_res + n_new == 0) go = false;    // empty after eviction: wait (R27)
       }
@@ -1120,6 +1424,7 @@ struct WarpSim {
         continue;
       }
       execute(n_evict, peak, waiting);
+      if (RING && status) break;
     }
     finish();
   }
@@ -1169,7 +1474,7 @@ struct WarpSim {
   }
 };
 
-template <int POL, bool TRACE>
+template <int POL, bool TRACE, bool RING>
 // WAIT: <= 4 warps per block, 5 blocks per SM -> <= 102 registers (20 warps/SM
 // at C2's shared-memory footprint); others are shared-memory bound: 128 regs
 __global__ void __launch_bounds__(POL == SCHED_WAIT ? 128 : 256, POL == SCHED_WAIT ? 5 : 2)
@@ -1179,7 +1484,7 @@ __global__ void __launch_bounds__(POL == SCHED_WAIT ? 128 : 256, POL == SCHED_WA
   const int lane = threadIdx.x & 31;
   const int slot = blockIdx.x * (blockDim.x >> 5) + wib;
   const size_t ring_base = (size_t)slot * P.n_rings * P.ring_cap;
-  WarpSim<POL, TRACE> sim(P, smem + (size_t)wib * P.warp_smem, lane, ring_base);
+  WarpSim<POL, TRACE, RING> sim(P, smem + (size_t)wib * P.warp_smem, lane, ring_base);
   for (;;) {
     uint32_t i = 0;
     if (lane == 0) i = atomicAdd(P.work_counter, 1u);
@@ -1197,18 +1502,18 @@ __global__ void __launch_bounds__(POL == SCHED_WAIT ? 128 : 256, POL == SCHED_WA
   }
 }
 
-template <int POL, bool TRACE>
+template <int POL, bool TRACE, bool RING = false>
 cudaError_t launch_t(const DevParams& p, int grid, int block, size_t smem, cudaStream_t s) {
-  auto k = sim_kernel<POL, TRACE>;
+  auto k = sim_kernel<POL, TRACE, RING>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<grid, block, smem, s>>>(p);
   return cudaGetLastError();
 }
 
-template <int POL, bool TRACE>
+template <int POL, bool TRACE, bool RING = false>
 cudaError_t occ_t(int block, size_t smem, int* bps) {
-  auto k = sim_kernel<POL, TRACE>;
+  auto k = sim_kernel<POL, TRACE, RING>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k, block, smem);
@@ -1226,6 +1531,13 @@ cudaError_t launch_sim(const DevParams& p, int grid, int block, size_t smem, cud
       default: return launch_t<SCHED_FCFS, true>(p, grid, block, smem, s);
     }
   }
+  if (p.ring_engine) {
+    switch (p.policy) {
+      case SCHED_WAIT: return launch_t<SCHED_WAIT, false, true>(p, grid, block, smem, s);
+      case SCHED_FCFS_ONGOING: return launch_t<SCHED_FCFS_ONGOING, false, true>(p, grid, block, smem, s);
+      default: return launch_t<SCHED_FCFS, false, true>(p, grid, block, smem, s);
+    }
+  }
   switch (p.policy) {
     case SCHED_WAIT: return launch_t<SCHED_WAIT, false>(p, grid, block, smem, s);
     case SCHED_NESTED: return launch_t<SCHED_NESTED, false>(p, grid, block, smem, s);
@@ -1234,7 +1546,14 @@ cudaError_t launch_sim(const DevParams& p, int grid, int block, size_t smem, cud
   }
 }
 
-cudaError_t sim_occupancy(int policy, int trace, int block, size_t smem, int* bps) {
+cudaError_t sim_occupancy(int policy, int trace, int block, size_t smem, int* bps, int ring) {
+  if (ring) {
+    switch (policy) {
+      case SCHED_WAIT: return occ_t<SCHED_WAIT, false, true>(block, smem, bps);
+      case SCHED_FCFS_ONGOING: return occ_t<SCHED_FCFS_ONGOING, false, true>(block, smem, bps);
+      default: return occ_t<SCHED_FCFS, false, true>(block, smem, bps);
+    }
+  }
   if (trace) {
     switch (policy) {
       case SCHED_WAIT: return occ_t<SCHED_WAIT, true>(block, smem, bps);

@@ -1,6 +1,6 @@
 # A/B: parity suite on the current build, then time each library on each workload
 # env: LIBS="base new" (paper_2504_11320_b200/libsched_<name>.so; "cur" = libsched.so), WLS="C2 C3a C4_2"
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+[ -n "$NOTEST" ] || { timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; }
 tail -3 gpurun_out/pytest_gpu.log
 : > gpurun_out/ab.log
 for wl in ${WLS:-C2 C3a C4_2}; do

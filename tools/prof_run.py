@@ -1,4 +1,5 @@
-"""One step of the bench workload (C2, WAIT then FCFS, 10^4 replications) for ncu."""
+"""One launch per policy of a workload for ncu (default: C2 WAIT + FCFS, 10^4 replications).
+env: WL=C2|C4_<i>|C3a|C3b|C5_55, POLS=comma list of policy names, REPS, HORIZON"""
 import os
 import sys
 
@@ -9,12 +10,29 @@ import workloads as W
 from paper_2504_11320_b200 import Scheduler
 from paper_2504_11320_b200.sim import run_rows
 
+wl_name = os.environ.get("WL", "C2")
+seg10 = [50 * k for k in range(1, 11)]
+if wl_name == "C2":
+    wl, pols = W.C2, [W.Policy(W.WAIT), W.Policy(W.FCFS, B=1024)]
+elif wl_name.startswith("C4_"):
+    wl = W.c4(int(wl_name[3:]))
+    pols = [W.Policy(W.WAIT), W.Policy(W.NESTED, seg_end=[100, 200, 300]), W.Policy(W.FCFS, B=1024)]
+elif wl_name == "C3a":
+    wl, pols = W.C3A, [W.Policy(W.NESTED, seg_end=[20, 40, 80, 160]), W.Policy(W.FCFS, B=1024)]
+elif wl_name == "C3b":
+    wl, pols = W.C3B, [W.Policy(W.NESTED, seg_end=seg10), W.Policy(W.FCFS, B=2048)]
+else:
+    wl, pols = W.c5(55.0), [W.Policy(W.NESTED, seg_end=seg10, thresholds=W.PAPER_NESTED_RATIO_C5),
+                            W.Policy(W.FCFS, B=1024)]
+if os.environ.get("POLS"):
+    keep = os.environ["POLS"].split(",")
+    pols = [p for p in pols if W.POLICY_NAMES[p.kind] in keep]
 R = int(os.environ.get("REPS", "10000"))
-T = float(os.environ.get("HORIZON", "10.0"))
-for pol in [W.Policy(W.WAIT), W.Policy(W.FCFS, B=1024)]:
-    s = Scheduler(W.C2, pol)
-    if pol.kind != W.FCFS:
+T = float(os.environ.get("HORIZON", str(wl.horizon_s)))
+for pol in pols:
+    s = Scheduler(wl, pol, pol.thresholds)
+    if pol.kind != W.FCFS and not pol.thresholds:
         s.thresholds()
-    rows = run_rows(s, W.C2.seed, 0, R, T)
+    rows = run_rows(s, wl.seed, 0, R, T)
     torch.cuda.synchronize()
-    print(pol.kind, s.launch_info(), int(rows[7].sum()))
+    print(W.POLICY_NAMES[pol.kind], s.launch_info(), int(rows[7].sum()))

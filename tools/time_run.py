@@ -47,4 +47,5 @@ for pol in pols:
     st = int((out[L.F["status"]] != 0).sum())
     li = s.launch_info()
     print(f"{wl_name} {W.POLICY_NAMES[pol.kind]:6s} ms={min(ts):8.3f} rs/s={rs/min(ts)*1e3:.3e} status!=0:{st} "
-          f"wpb={li['warps_per_block']} bps={li['blocks_per_sm']} Rc={li['max_resident']} smem={li['shared_bytes']}")
+          f"wpb={li['warps_per_block']} bps={li['blocks_per_sm']} spec={li['spec_resident']} safe={li['max_resident']} "
+          f"smem={li['shared_bytes']} fb={li['fallback_grid']} eng={li.get('engine', 0)}")
