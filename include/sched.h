@@ -194,9 +194,11 @@ typedef struct {
   int32_t engine;                         /* 0 member engine (per-resident records, every
                                              policy); 1 class-ring engine (WAIT / FCFS with
                                              fixed per-class lengths; capacities
-                                             then count ring + staging records).  The env var
-                                             WAITSIM_ENGINE=member (read at the first run)
-                                             forces the member engine. */
+                                             then count ring + staging records).  Chosen
+                                             automatically (ring unless its footprint exceeds
+                                             the member engine's by > 30%); the env var
+                                             WAITSIM_ENGINE=member|ring, read when the handle
+                                             is first launched, forces one. */
 } sched_launch_info;
 int sched_get_launch_info(sched_t h, sched_launch_info* out);
 

@@ -294,7 +294,23 @@ int prepare(sched_s* h) {
       L.Rc = std::min<uint32_t>(L.Rc_safe, round32((uint64_t)(1.5 * adm) + 64));
     }
     if (int rc = size_cfg(L)) return rc;
-    h->use_ring = true;
+    // the ring engine does O(classes + events) work per batch but its
+    // per-class capacities can cost occupancy: keep it unless its
+    // speculative footprint exceeds the member engine's by > 30%
+    // (measured: C2, C4 rho=0.5/0.8 WAIT and C2 FCFS gain; C4 rho=0.95 WAIT
+    // and long-l' FCFS lose)
+    uint64_t ring_rec = L.Rc + 32;
+    for (int c = 0; c < K; ++c) ring_rec += L.rcap[c];
+    // FCFS additionally only for short decodes: with l' >> 1 most of an FCFS
+    // batch is the fixed per-batch control both engines share and the ring
+    // engine's lower occupancy loses (measured: C2 l' <= 20 +13%, C4 l' >=
+    // 100 -5..-12%)
+    double lam = 0, lam_lp = 0;
+    for (int c = 0; c < K; ++c) { lam += in.lambda[c]; lam_lp += in.lambda[c] * in.lp[c][0].first; }
+    const bool short_lp = lam > 0 && lam_lp / lam <= 64.0;
+    const bool forced = eng && std::string(eng) == "ring";
+    h->use_ring = forced || h->max_resident_cfg || h->spec_resident_cfg ||
+                  ((double)ring_rec <= 1.3 * (double)h->mem.Rc && (in.policy == SCHED_WAIT || short_lp));
   }
   const int n_rings = h->in.policy == SCHED_WAIT ? K : 1;
   size_t slots = (size_t)std::max(h->mem.grid * h->mem.wpb, h->mem.fb_grid * h->mem.fb_wpb);

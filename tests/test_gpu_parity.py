@@ -304,3 +304,41 @@ def test_degenerate_horizons_and_capacity():
                       horizon_s=1.0, seed=1)
     rows = check(zero, W.Policy(W.FCFS, B=2), [0], 4)
     assert (rows[oracle.F["arrivals"]] == 0).all()
+
+
+# ------------------------------------------- both engines, every eligible case
+@pytest.mark.parametrize("engine", ["member", "ring"])
+@pytest.mark.parametrize("case", ["c2_wait", "c2_fcfs", "c2_ongoing", "c4_wait_evict", "c4_fcfs_evict",
+                                  "c1_wait_evict", "random_wait", "random_fcfs"])
+def test_engines_bit_exact(engine, case, monkeypatch):
+    """The member engine and the class-ring engine are two
+    layouts of one semantics: forced either way, every row matches the
+    oracle, including the LIFO-eviction regime (batched ring eviction) and
+    pending first tokens of evicted prompts."""
+    from paper_2504_11320_b200 import Scheduler
+    monkeypatch.setenv("WAITSIM_ENGINE", engine)
+    rng = np.random.default_rng(77)
+    if case.startswith("c2"):
+        kind = {"c2_wait": W.WAIT, "c2_fcfs": W.FCFS, "c2_ongoing": W.FCFS_ONGOING}[case]
+        wl, pol, thr, n, T = W.C2, W.Policy(kind, B=1024), ([16, 16] if kind == W.WAIT else [0]), 24, 2.0
+    elif case == "c4_wait_evict":
+        wl, pol, thr, n, T = W.c4(3), W.Policy(W.WAIT), [9, 6, 3], 12, 8.0
+    elif case == "c4_fcfs_evict":
+        wl, pol, thr, n, T = W.c4(4), W.Policy(W.FCFS, B=1024), [0], 12, 8.0
+    elif case == "c1_wait_evict":
+        wl, pol, thr, n, T = W.C1, W.Policy(W.WAIT), [1], 32, W.C1.horizon_s
+    else:
+        wl = W.random_small(rng, horizon_s=2.0)
+        while any(len(x) > 1 for x in wl.l_tab + wl.lp_tab):  # fixed lengths: ring-eligible
+            wl = W.random_small(rng, horizon_s=2.0)
+        kind = W.WAIT if case == "random_wait" else W.FCFS
+        pol = W.Policy(kind, B=64)
+        thr = [int(x) for x in rng.integers(1, 4, size=wl.K)] if kind == W.WAIT else [0]
+        n, T = 32, 2.0
+    s = Scheduler(wl, pol, None if pol.kind in (W.FCFS, W.FCFS_ONGOING) else thr)
+    assert s.launch_info()["engine"] == (1 if engine == "ring" else 0)
+    got = s.run_host(wl.seed, 0, n, T)
+    s.close()
+    ref = oracle.run(wl, pol, thr, n_reps=n, n_threads=8, horizon_s=T)
+    assert_rows_equal(got, ref, f"{case}/{engine}")
+    assert (got[oracle.F["status"]] == 0).all()
