@@ -100,7 +100,9 @@ typedef struct {
                                  seg_end[0] >= 1, seg_end[L-1] >= max l' */
   uint32_t B;                 /* FCFS*: max resident prompts (>= 1); WAIT heuristic B */
   uint32_t tok_budget;        /* FCFS*: max prefill tokens per iteration (0 = none) */
-  uint32_t max_resident;      /* per-replication resident capacity (0 = derive) */
+  uint32_t max_resident;      /* per-replication safe resident capacity (0 = derive): the
+                                 fallback launch's; the main launch still runs with a
+                                 speculative capacity <= it (see spec_resident) */
   uint32_t restart_cap;       /* per-FIFO restart ring capacity (0 = default 8192) */
   /* optional time-varying rates ("Time-Varying Arrival
    * Rates"; NULL rf_off = all homogeneous): class c has pieces

@@ -100,7 +100,6 @@ uint32_t round32(uint64_t x) { return (uint32_t)((std::max<uint64_t>(x, 32) + 31
 // with the safe capacity (derive_rc) by the fallback launch
 uint32_t speculative_rc(const sched_s* h, uint32_t safe) {
   if (h->spec_resident_cfg) return std::min(safe, round32(h->spec_resident_cfg));
-  if (h->max_resident_cfg) return safe;
   const auto& in = h->in;
   uint64_t rc = safe;
   if (is_fcfs(in.policy)) {
@@ -115,6 +114,28 @@ uint32_t speculative_rc(const sched_s* h, uint32_t safe) {
       prev = in.seg_end[k];
     }
     rc = base + 64;
+  }
+  if (!is_fcfs(in.policy) || h->n_star_total == 0) {
+    // memory caps the population: a resident holds l + s - 1 KV tokens, on
+    // average (time-weighted over its l' + 1 iterations) E[(l'+1)(l + l'/2)]
+    // / E[l'+1] (R26), so ~ M / that residents + margin
+    double num = 0, den = 0;
+    for (size_t c = 0; c < in.lambda.size(); ++c) {
+      double wl = 0, el = 0, wp = 0, ep1 = 0, eq = 0;
+      for (auto& e : in.l[c]) { wl += (double)e.second; el += (double)e.second * e.first; }
+      for (auto& e : in.lp[c]) {
+        const double y = e.first;
+        wp += (double)e.second;
+        ep1 += (double)e.second * (y + 1);
+        eq += (double)e.second * (y + 1) * y / 2;
+      }
+      if (wl <= 0 || wp <= 0) continue;
+      el /= wl; ep1 /= wp; eq /= wp;
+      num += in.lambda[c] * (ep1 * el + eq);
+      den += in.lambda[c] * ep1;
+    }
+    if (num > 0 && den > 0)
+      rc = std::min<uint64_t>(rc, (uint64_t)(1.4 * (double)in.M / (num / den)) + 96);
   }
   return std::min(safe, round32(rc));
 }
@@ -279,7 +300,7 @@ int prepare(sched_s* h) {
         L.rcap[c] = std::max<uint32_t>(1, std::min<uint32_t>(L.rcap_safe[c],
                        (uint32_t)((uint64_t)h->spec_resident_cfg * L.rcap_safe[c] / std::max<uint64_t>(1, safe_tot))));
       L.Rc = std::min<uint32_t>(L.Rc_safe, std::max<uint32_t>(32, h->spec_resident_cfg / 4));
-    } else if (is_fcfs(in.policy) && !h->max_resident_cfg && h->n_star_total > 0) {
+    } else if (is_fcfs(in.policy) && h->n_star_total > 0) {
       // FCFS residents ~ fluid prompts in service n*_c, scaled
       // by M / M* when memory binds and by B / n* when the batch cap binds
       // (WAIT needs no speculation: n_c per stage exactly, P14)
@@ -309,7 +330,7 @@ int prepare(sched_s* h) {
     for (int c = 0; c < K; ++c) { lam += in.lambda[c]; lam_lp += in.lambda[c] * in.lp[c][0].first; }
     const bool short_lp = lam > 0 && lam_lp / lam <= 64.0;
     const bool forced = eng && std::string(eng) == "ring";
-    h->use_ring = forced || h->max_resident_cfg || h->spec_resident_cfg ||
+    h->use_ring = forced || h->spec_resident_cfg ||
                   ((double)ring_rec <= 1.3 * (double)h->mem.Rc && (in.policy == SCHED_WAIT || short_lp));
   }
   const int n_rings = h->in.policy == SCHED_WAIT ? K : 1;

@@ -25,11 +25,16 @@ elif wl_name.startswith("C4_"):
 elif wl_name == "C3b":
     wl, pols = W.C3B, [W.Policy(W.NESTED, seg_end=seg10), W.Policy(W.FCFS, B=2048)]
 else:
-    wl, pols = W.c5(55.0), [W.Policy(W.NESTED, seg_end=seg10, thresholds=W.PAPER_NESTED_RATIO_C5), W.Policy(W.FCFS, B=1024)]
+    wl, pols = W.c5(55.0), [W.Policy(W.NESTED, seg_end=seg10), W.Policy(W.FCFS, B=1024)]
 R = int(os.environ.get("REPS", "10000"))
 T = float(os.environ.get("HORIZON", str(wl.horizon_s)))
 for pol in pols:
-    s = Scheduler(wl, pol, pol.thresholds)
+    kw = {}
+    if os.environ.get("RCAP"):
+        kw["restart_cap"] = int(os.environ["RCAP"])
+    if os.environ.get("MAXRES"):
+        kw["max_resident"] = int(os.environ["MAXRES"])
+    s = Scheduler(wl, pol, pol.thresholds, **kw)
     if pol.kind != W.FCFS and not pol.thresholds:
         s.thresholds()
     out = torch.empty((L.NF, R), dtype=torch.int64, device="cuda")
