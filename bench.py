@@ -393,7 +393,8 @@ def main():
 
     # roofline of the dominant kernel (alu/issue bound),
     # timed alone (no concurrent launches) on its own stream
-    dom = max(units, key=lambda n: units[n]["request_steps"])
+    # dominant = the launch with the largest device time in the timed steps
+    dom = max(t_kern, key=lambda n: sum(t_kern[n]))
     di = [n for n, _, _ in scheds].index(dom)
     _, s_dom, wl_dom = scheds[di]
     solo = []
