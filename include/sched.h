@@ -117,6 +117,10 @@ typedef struct {
                                  replications exceeding it are re-run with the safe
                                  capacity by a fallback launch on the same stream */
   int32_t device;             /* CUDA device ordinal */
+  int64_t tau_b0;             /* piecewise-linear iteration time (DESIGN.md
+                                 R31): tau = d0 + d1 * max(0, tokens - tau_b0); 0 = the
+                                 linear Eq. time_consump; >= 0.  Threshold setup
+                                 (sched_thresholds) keeps the linear model. */
 } sched_config;
 
 /* Validate and copy *cfg (every array is copied; cfg may be freed after),

@@ -58,7 +58,7 @@ class _Cfg(C.Structure):
         ("n_seg", C.c_int32), ("seg_end", C.POINTER(C.c_uint16)),
         ("B", C.c_uint32), ("tok_budget", C.c_uint32), ("horizon_s", C.c_double),
         ("rf_off", C.POINTER(C.c_int32)), ("rf_t", C.POINTER(C.c_double)),
-        ("rf_rate", C.POINTER(C.c_double)),
+        ("rf_rate", C.POINTER(C.c_double)), ("tau_b0", C.c_int64),
     ]
 
 
@@ -129,6 +129,7 @@ class Config:
         cfg.seg_end, cfg.n_seg = p, len(seg)
         cfg.B, cfg.tok_budget = policy.B, policy.tok_budget
         cfg.horizon_s = wl.horizon_s if horizon_s is None else horizon_s
+        cfg.tau_b0 = int(getattr(wl, "tau_b0", 0))
         rfs = getattr(wl, "rate_fn", None)
         if rfs:
             off, ts, rs = [0], [], []

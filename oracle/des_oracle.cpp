@@ -170,7 +170,7 @@ struct Setup {  // per-config constants, recomputed here from the raw config
   std::vector<RatePieces> rf;      // time-varying classes (empty = homogeneous)
   std::vector<double> gap_scale;   // 1e12 / lambda_c, ticks per unit exponential
   std::vector<LenTable> ltab, lptab;
-  int64_t d0_t, d1_t, T_t, M;
+  int64_t d0_t, d1_t, T_t, M, b0 = 0;
   std::vector<uint32_t> thr;
   std::vector<int> seg_end;
   uint32_t B, tok_budget;
@@ -190,6 +190,7 @@ struct Setup {  // per-config constants, recomputed here from the raw config
     // 1 tick = 1 ps
     d0_t = std::llround(cfg->d0_s * 1e12);
     d1_t = std::llround(cfg->d1_s * 1e12);
+    b0 = cfg->tau_b0;
     T_t = std::llround(cfg->horizon_s * 1e12);
     M = cfg->M;
     thr.assign(cfg->thr, cfg->thr + cfg->n_thr);
@@ -456,7 +457,8 @@ struct Sim {
           for (uint64_t x = 0; x < popped[q]; ++x) fifo[q].pop_front();
       }
       for (const Prompt& p : fresh) tokens += p.l;
-      const int64_t tau = S.d0_t + S.d1_t * tokens;
+      // ... piecewise linear beyond b0 tokens (b0 = 0: Eq. time_consump)
+      const int64_t tau = S.d0_t + S.d1_t * std::max<int64_t>(0, tokens - S.b0);
       const int64_t t_end = now + tau;
       uint64_t n_complete = 0;
       std::vector<Prompt> kept;

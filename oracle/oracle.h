@@ -51,6 +51,9 @@ typedef struct {
   const int32_t* rf_off;
   const double* rf_t;
   const double* rf_rate;
+  /* piecewise-linear iteration time (reading R31):
+   * tau = d0 + d1 * max(0, tokens - tau_b0); 0 = the linear Eq. time_consump */
+  int64_t tau_b0;
 } orc_config;
 
 /* Philox4x32-10 (Salmon et al. SC'11). */

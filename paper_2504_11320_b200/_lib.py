@@ -57,7 +57,7 @@ class SchedConfig(C.Structure):
         ("restart_cap", C.c_uint32),
         ("rf_off", C.POINTER(C.c_uint32)), ("rf_t", C.POINTER(C.c_double)),
         ("rf_rate", C.POINTER(C.c_double)),
-        ("spec_resident", C.c_uint32), ("device", C.c_int32),
+        ("spec_resident", C.c_uint32), ("device", C.c_int32), ("tau_b0", C.c_int64),
     ]
 
 
@@ -176,6 +176,7 @@ class Scheduler:
         cfg.B, cfg.tok_budget = policy.B, policy.tok_budget
         cfg.max_resident, cfg.restart_cap, cfg.device = max_resident, restart_cap, device
         cfg.spec_resident = spec_resident
+        cfg.tau_b0 = int(getattr(workload, "tau_b0", 0))
         rfs = getattr(workload, "rate_fn", None)
         if rfs:
             off, ts, rs = [0], [], []

@@ -431,6 +431,7 @@ int sched_create(sched_t* out, const sched_config* cfg) {
     return fail(SCHED_E_INVALID, "null table pointer");
   if (!(cfg->d0_s > 0) || !(cfg->d1_s >= 0)) return fail(SCHED_E_INVALID, "need d0 > 0, d1 >= 0");
   if (cfg->M < 1) return fail(SCHED_E_INVALID, "M must be >= 1");
+  if (cfg->tau_b0 < 0) return fail(SCHED_E_INVALID, "tau_b0 must be >= 0");
   if (cfg->policy < SCHED_WAIT || cfg->policy > SCHED_FCFS_ONGOING) return fail(SCHED_E_INVALID, "bad policy");
   sched_s* h = new sched_s();
   SetupInput& in = h->in;
@@ -557,6 +558,7 @@ int sched_create(sched_t* out, const sched_config* cfg) {
   p.M = cfg->M;
   p.B = cfg->B;
   p.tok_budget = cfg->tok_budget;
+  p.b0 = cfg->tau_b0;
   h->h_cdf_thr = std::move(thr_all);
   h->h_cdf_val = std::move(val_all);
   if (cfg->policy == SCHED_NESTED) {

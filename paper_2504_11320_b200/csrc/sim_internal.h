@@ -23,6 +23,7 @@ struct DevParams {
   int32_t n_rings;         // restart rings per replication (WAIT: K, else 1)
   int32_t n_seg;
   int64_t d0_t, d1_t, T_t, M;
+  int64_t b0;              // piecewise-linear iteration time threshold (tokens; 0 = linear)
   uint32_t thr[kMaxSegments];      // WAIT: per class, NESTED: per segment
   uint32_t B, tok_budget;
   uint32_t Rc;             // resident capacity per replication (class-ring engine: staging capacity)

@@ -1333,8 +1333,9 @@ struct WarpSim {
                            uint32_t nf, uint32_t dtok, uint32_t kvf, uint32_t gr, uint64_t done_a,
                            uint64_t ft_a) {
     const int64_t tokens = (int64_t)tok + sum_new_l;
-    // tau = d0 + d1 * (sum prefill l + sum decode (l+s))
-    const int64_t tau = P.d0_t + P.d1_t * tokens;
+    // tau = d0 + d1 * (sum prefill l + sum decode (l+s)),
+    // piecewise linear beyond b0 tokens (R31; b0 = 0: linear)
+    const int64_t tau = P.d0_t + P.d1_t * max(tokens - P.b0, (int64_t)0);
     const int64_t t_end = now + tau;
     const bool by_T = t_end <= P.T_t;
     if (by_T) { acc_done_a += done_a; acc_ft_a += ft_a; }

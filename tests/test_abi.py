@@ -39,7 +39,7 @@ def test_no_oracle_in_product_path():
 
 @pytest.mark.parametrize("bad", [
     dict(lam=[-1.0]), dict(M=0), dict(d0_s=0.0), dict(l_tab=[[(0, 1)]]),
-    dict(lp_tab=[[(5, 0)]]), dict(lp_tab=[[(300, 1)]]),
+    dict(lp_tab=[[(5, 0)]]), dict(lp_tab=[[(300, 1)]]), dict(tau_b0=-1),
 ])
 def test_create_validation(bad):
     base = dict(lam=[10.0], l_tab=[W.fixed(4)], lp_tab=[W.fixed(8)], M=256, horizon_s=1.0, seed=1)

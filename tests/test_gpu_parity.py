@@ -342,3 +342,22 @@ def test_engines_bit_exact(engine, case, monkeypatch):
     ref = oracle.run(wl, pol, thr, n_reps=n, n_threads=8, horizon_s=T)
     assert_rows_equal(got, ref, f"{case}/{engine}")
     assert (got[oracle.F["status"]] == 0).all()
+
+
+# ------------------------------- piecewise-linear iteration time
+@pytest.mark.parametrize("engine", ["member", "ring"])
+def test_piecewise_linear_tau(engine, monkeypatch):
+    """tau = d0 + d1 max(0, tokens - b0) (reading R31), both engines, C2 with
+    b0 inside the batch-token range, and random small systems."""
+    import dataclasses
+    monkeypatch.setenv("WAITSIM_ENGINE", engine)
+    for b0 in [3000, 8000]:
+        wl = dataclasses.replace(W.C2, tau_b0=b0)
+        check(wl, W.Policy(W.WAIT), [16, 16], 16, horizon_s=2.0)
+        check(wl, W.Policy(W.FCFS, B=1024), [0], 16, horizon_s=2.0)
+    rng = np.random.default_rng(4242)
+    for _ in range(6):
+        wl = dataclasses.replace(W.random_small(rng, horizon_s=1.5), tau_b0=int(rng.integers(0, 40)))
+        seg = [max(max(v for v, _ in t) for t in wl.lp_tab)]
+        check(wl, W.Policy(W.NESTED, seg_end=seg), [2], 16)
+        check(wl, W.Policy(W.FCFS, B=64), [0], 16)

@@ -371,6 +371,47 @@ def test_fcfs_b1_is_md1():
     assert int(rows[F["first_tokens"], 0]) == nft
 
 
+@pytest.mark.parametrize("b0", [0, 7, 100])
+def test_piecewise_linear_tau_fcfs_b1(b0):
+    """Piecewise-linear iteration time tau = d0 + d1 max(0, tokens - b0)
+    (reading R31) on the P9 system (FCFS, B=1, ample memory):
+    one prompt at a time, E_i = max(E_{i-1}, a_i) + sum_s (d0 + d1 max(0,
+    l + s - b0)) [derived]; b0 = 7 cuts inside the stage range (tokens 5..9),
+    b0 = 100 leaves the constant overhead d0 only (constant service time)."""
+    wl = W.Workload("md1pw", [30.0], [W.fixed(5)], [W.fixed(4)], M=10 ** 6, horizon_s=20.0, seed=5,
+                    tau_b0=b0)
+    d0, d1, T = round(wl.d0_s * TPS), round(wl.d1_s * TPS), round(wl.horizon_s * TPS)
+    t, _, _ = oracle.gen_arrivals(wl, 0, 0, 2000)
+    a = [x for x in t.tolist() if x < T]
+    E, done, lat, batches, busy = 0, 0, 0, 0, 0
+    for x in a:
+        s = max(E, x)
+        ends = []
+        for st in range(5):
+            if s >= T:
+                break
+            tau = d0 + d1 * max(0, 5 + st - b0)
+            s += tau
+            busy += tau
+            ends.append(s)
+            batches += 1
+        if len(ends) == 5:
+            E = ends[-1]
+            if E <= T:
+                done += 1
+                lat += E - x
+        else:
+            break
+    rows = oracle.run(wl, W.Policy(W.FCFS, B=1), [0])
+    assert int(rows[F["completed"], 0]) == done
+    assert int(rows[F["batches"], 0]) == batches
+    assert int(rows[F["busy_ticks"], 0]) == busy
+    assert oracle.u128(rows, "lat")[0] == lat
+    if b0 == 0:  # reduces to the linear model exactly
+        base = W.Workload("md1", [30.0], [W.fixed(5)], [W.fixed(4)], M=10 ** 6, horizon_s=20.0, seed=5)
+        assert np.array_equal(rows, oracle.run(base, W.Policy(W.FCFS, B=1), [0]))
+
+
 def test_nested_one_segment_equals_wait():
     """P10: Nested WAIT with a single segment is WAIT with one type."""
     for wl, n in [(W.C1, 1), (W.C1P, 1), (W.C1, 2)]:

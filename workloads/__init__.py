@@ -60,6 +60,9 @@ class Workload:
     # optional time-varying rates: per class a list of
     # (start second, rate) pieces, first start 0; None / [] = constant lam
     rate_fn: Optional[List[Optional[List[Tuple[float, float]]]]] = None
+    # piecewise-linear iteration time tau = d0 + d1 max(0, tokens - tau_b0)
+    # (reading R31); 0 = the linear model
+    tau_b0: int = 0
 
     @property
     def K(self) -> int:
