@@ -115,7 +115,7 @@ uint32_t speculative_rc(const sched_s* h, uint32_t safe) {
     }
     rc = base + 64;
   }
-  if (!is_fcfs(in.policy) || h->n_star_total == 0) {
+  if (in.policy == SCHED_NESTED) {
     // memory caps the population: a resident holds l + s - 1 KV tokens, on
     // average (time-weighted over its l' + 1 iterations) E[(l'+1)(l + l'/2)]
     // / E[l'+1] (R26), so ~ M / that residents + margin

@@ -307,6 +307,7 @@ struct WarpSim {
   uint32_t Qmask;     // WAIT: qualifying classes
   int kstar;          // NESTED: last active segment
   uint32_t n_plan_res;
+  bool below;         // no batch because of the threshold test (idle skip allowed)
 
   __device__ WarpSim(const DevParams& p, unsigned char* base, int lane_, size_t rb)
       : P(p), lane(lane_), ring_base(rb) {
@@ -456,6 +457,42 @@ struct WarpSim {
       if (t < P.T_t && t < best) best = t;
     }
     return best;
+  }
+
+  __device__ __forceinline__ static int64_t warp_min_i64(int64_t x) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) x = min(x, (int64_t)__shfl_xor_sync(FULL, (long long)x, d));
+    return x;
+  }
+
+  // Idle skip.  While no batch can start because of the threshold test
+  // (WAIT: no type has n_j waiting, line 1488; NESTED: fewer than n_1 wait,
+  // line 1640), residents do not move and only arrivals change the decision,
+  // so the epochs at the intermediate arrivals are no-ops whose idle time
+  // adds up (DESIGN.md §4.4 step 3): jump straight to the arrival that can
+  // start a batch.  Exact within the generated windows, else to the last
+  // arrival every window still holds (an earlier epoch; ingest refills).
+  __device__ int64_t idle_jump() const {
+    int64_t bound = lane < P.K ? vt[lane * 32 + 31] : TMAX;
+    if (POL == SCHED_WAIT) {
+      int64_t cand = TMAX;
+      if (lane < P.K) {
+        const uint32_t q = k_vis - k_adm + (rtail - rhead);  // < n_j (type not qualifying)
+        const uint32_t j = (k_vis - vbase) + (P.thr[lane] - q) - 1;
+        cand = j < 32 ? vt[lane * 32 + j] : bound;
+      }
+      return warp_min_i64(cand);
+    } else {
+      bound = warp_min_i64(bound);
+      uint32_t d = P.thr[0] - waiting_total();  // >= 1 arrivals still needed
+      uint32_t ptr = lane < P.K ? k_vis - vbase : 32u;
+      for (;;) {
+        const int64_t h = ptr < 32 ? vt[lane * 32 + ptr] : TMAX;
+        const int64_t m = warp_min_i64(h);
+        if (m >= bound || --d == 0) return min(m, bound);
+        if ((uint32_t)lane == (uint32_t)__ffs(__ballot_sync(FULL, h == m)) - 1) ++ptr;
+      }
+    }
   }
 
   __device__ uint32_t waiting_total() const {
@@ -807,6 +844,7 @@ struct WarpSim {
   __device__ bool decide() {
     n_new = 0;
     sum_new_l = 0;
+    below = false;
     if (POL == SCHED_WAIT) {
       // Algorithm 1: type j joins the batch iff n_j0 >= n_j;
       // all residents of qualifying types ride along (line 1490, invariant P14)
@@ -816,14 +854,14 @@ struct WarpSim {
         if (w >= P.thr[lane]) { qq = 1; npr = RING ? r_n : cnt[lane]; }
       }
       Qmask = __ballot_sync(FULL, qq);
-      if (!Qmask) return false;
+      if (!Qmask) { below = true; return false; }
       n_plan_res = __reduce_add_sync(FULL, npr);
       save_cursors();
       return take_wait(0xFFFFFFFFu);
     } else if (POL == SCHED_NESTED) {
       // Algorithm 2: largest k with Q_{k',entry} >= n_k' for all k' <= k
       // (PAPER.md:1640); batch min{n_k, Q_{k,s}} per stage (line 1642)
-      if (waiting_total() < P.thr[0]) return false;
+      if (waiting_total() < P.thr[0]) { below = true; return false; }
       const bool pass = lane >= 1 && lane < P.n_seg && cnt[32 + lane] >= P.thr[lane];
       const uint32_t fail = ~__ballot_sync(FULL, pass) & ~1u;  // bit 0 = segment 1 (passed)
       const int ks = min(__ffs(fail) - 2, P.n_seg - 1);
@@ -1418,7 +1456,8 @@ struct WarpSim {
         if (n_plan_res + n_new == 0) go = false;    // empty after eviction: wait (R27)
       }
       if (!go) {
-        const int64_t nt = next_arrival();
+        int64_t nt = (POL == SCHED_WAIT || POL == SCHED_NESTED) && below ? idle_jump() : TMAX;
+        if (nt >= P.T_t) nt = next_arrival();  // near the horizon: step arrival by arrival
         if (nt == TMAX) break;
         if (lane == 0) st->idle += nt - now;
         now = nt;

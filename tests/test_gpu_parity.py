@@ -361,3 +361,15 @@ def test_piecewise_linear_tau(engine, monkeypatch):
         seg = [max(max(v for v, _ in t) for t in wl.lp_tab)]
         check(wl, W.Policy(W.NESTED, seg_end=seg), [2], 16)
         check(wl, W.Policy(W.FCFS, B=64), [0], 16)
+
+
+def test_idle_skip_partial_jumps():
+    """Idle skip: thresholds above the 32-arrival window force
+    jumps to the window bound (partial), multi-class merges and ties at the
+    horizon; rows stay bit-exact."""
+    wl = W.Workload("skip", [40.0, 25.0, 90.0], [W.fixed(3), W.fixed(5), W.fixed(2)],
+                    [W.fixed(4), W.fixed(9), W.fixed(2)], M=4000, horizon_s=6.0, seed=99)
+    check(wl, W.Policy(W.WAIT), [40, 33, 70], 16)
+    check(wl, W.Policy(W.WAIT), [1, 2, 3], 16)
+    check(wl, W.Policy(W.NESTED, seg_end=[2, 9]), [45, 20], 16)
+    check(wl, W.Policy(W.NESTED, seg_end=[2, 9]), [3, 2], 16)
