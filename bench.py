@@ -318,16 +318,25 @@ def main():
     F_ = pkg.F
 
     # every policy's launch on its own stream, so independent launches share
-    # the GPU (a C4 sweep point alone does not fill 148 SMs)
-    pstreams = [torch.cuda.Stream(dev) for _ in scheds]
+    # the GPU (a C4 sweep point alone does not fill 148 SMs); launches that
+    # each fill the GPU for >= 2 waves run back to back on one stream instead
+    # (concurrent persistent grids only fragment each other's occupancy)
+    def waves(s, n):
+        li = s.launch_info()
+        return n / max(1, li["grid"] * li["warps_per_block"])
+    n_local = D.rep_range(0, rank, world, R)[1]
+    serial = all(waves(s, n_local) >= 2.0 for _, s, _ in scheds)
+    pstreams = [torch.cuda.Stream(dev)] * len(scheds) if serial else [torch.cuda.Stream(dev) for _ in scheds]
 
-    def step(k, ev_start=None, ev_ends=None):
+    def step(k, ev_start=None, ev_ends=None, ev_begins=None):
         begin, n = D.rep_range(k, rank, world, R)
         start = ev_start or torch.cuda.Event()
         start.record(stream)
         ends = ev_ends or [torch.cuda.Event() for _ in scheds]
         for i, (name, s, wl) in enumerate(scheds):
             pstreams[i].wait_event(start)
+            if ev_begins:
+                ev_begins[i].record(pstreams[i])
             run_rows(s, wl.seed, begin, n, wl.horizon_s, rows[name], pstreams[i])
             ends[i].record(pstreams[i])
         for e in ends:
@@ -350,13 +359,14 @@ def main():
         flush.zero_()
         ev0 = torch.cuda.Event(enable_timing=True)
         ends = [torch.cuda.Event(enable_timing=True) for _ in scheds]
+        begins = [torch.cuda.Event(enable_timing=True) for _ in scheds]
         ev1 = torch.cuda.Event(enable_timing=True)
-        agg = step(k, ev0, ends)
+        agg = step(k, ev0, ends, begins)
         ev1.record(stream)
         torch.cuda.synchronize()
         t_step.append(ev0.elapsed_time(ev1) / 1e3)
         for i, (n, _, _) in enumerate(scheds):
-            t_kern[n].append(ev0.elapsed_time(ends[i]) / 1e3)  # concurrent: start -> its end
+            t_kern[n].append(begins[i].elapsed_time(ends[i]) / 1e3)  # this launch: begin -> end
             r = rows[n]
             for u in units[n]:
                 units[n][u] += int(r[F_[u]].sum().item())
@@ -445,8 +455,9 @@ def main():
                      "peak_basis": f"{props.multi_processor_count} SMs x 4 warp-instr/clk x 32 lanes x "
                                    f"{sm_max:.0f} MHz ({peak_src})"},
         "kernel_ms": {n: 1e3 * sum(v) / len(v) for n, v in t_kern.items()},
-        "kernel_ms_note": "per policy: step start -> that launch's end (launches run concurrently on "
-                          "separate streams); roofline uses the dominant launch timed alone",
+        "kernel_ms_note": "per policy: that launch's begin -> end (" + (
+            "launches run back to back on one stream: each fills the GPU for >= 2 waves" if serial else
+            "launches run concurrently on separate streams") + "); roofline uses the dominant launch timed alone",
         "dominant_alone_ms": 1e3 * dur,
         "clocks": clk,
     }

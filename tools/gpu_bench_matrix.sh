@@ -5,7 +5,7 @@ cat gpurun_out/bench_default.json >> gpurun_out/bench_matrix.jsonl
 for w in C1 C3a C3a_tv C3b C4; do
   timeout 900 python bench.py --workload $w --steps 5 --warmup 3 >> gpurun_out/bench_matrix.jsonl 2>> gpurun_out/bench_matrix.err
 done
-timeout 1500 python bench.py --workload C5 --steps 2 --warmup 1 --reps 512 --cpu-reps 4 >> gpurun_out/bench_matrix.jsonl 2>> gpurun_out/bench_matrix.err
+timeout 1500 python bench.py --workload C5 --steps 2 --warmup 3 --cpu-reps 16 >> gpurun_out/bench_matrix.jsonl 2>> gpurun_out/bench_matrix.err
 timeout 600 python bench.py --workload walks --steps 5 --warmup 2 >> gpurun_out/bench_matrix.jsonl 2>> gpurun_out/bench_matrix.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.json 2>> gpurun_out/bench_matrix.err
 python - <<'PY'
