@@ -57,9 +57,10 @@ struct sched_s {
   // device-side tables
   uint64_t* d_cdf_thr = nullptr;
   uint16_t* d_cdf_val = nullptr;
+  uint16_t* d_cdf_guide = nullptr;
   uint8_t* d_stage_info = nullptr;
   std::vector<uint64_t> h_cdf_thr;     // uploaded lazily by prepare()
-  std::vector<uint16_t> h_cdf_val;
+  std::vector<uint16_t> h_cdf_val, h_cdf_guide;
   std::vector<uint8_t> h_stage_info;
   std::vector<int64_t> h_rf_B, h_rf_Lam;   // time-varying rate pieces
   std::vector<double> h_rf_scale;
@@ -178,6 +179,9 @@ int prepare(sched_s* h) {
     CK(cudaMalloc(&h->d_cdf_val, h->h_cdf_val.size() * 2));
     CK(cudaMemcpy(h->d_cdf_thr, h->h_cdf_thr.data(), h->h_cdf_thr.size() * 8, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->d_cdf_val, h->h_cdf_val.data(), h->h_cdf_val.size() * 2, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&h->d_cdf_guide, h->h_cdf_guide.size() * 2));
+    CK(cudaMemcpy(h->d_cdf_guide, h->h_cdf_guide.data(), h->h_cdf_guide.size() * 2, cudaMemcpyHostToDevice));
+    h->base.cdf_guide = h->d_cdf_guide;
     if (!h->h_stage_info.empty()) {
       CK(cudaMalloc(&h->d_stage_info, h->h_stage_info.size()));
       CK(cudaMemcpy(h->d_stage_info, h->h_stage_info.data(), h->h_stage_info.size(), cudaMemcpyHostToDevice));
@@ -438,7 +442,7 @@ int sched_create(sched_t* out, const sched_config* cfg) {
   in.d0_s = cfg->d0_s; in.d1_s = cfg->d1_s; in.M = cfg->M; in.policy = cfg->policy; in.B = cfg->B;
   uint32_t max_lp = 0, min_l = 0xFFFF, max_l = 0;
   std::vector<uint64_t> thr_all;
-  std::vector<uint16_t> val_all;
+  std::vector<uint16_t> val_all, guide_all;
   for (uint32_t c = 0; c < K; ++c) {
     if (!(cfg->lambda[c] >= 0) || std::isinf(cfg->lambda[c])) { delete h; return fail(SCHED_E_INVALID, "lambda must be finite and >= 0"); }
     if (!table_ok(cfg->l_off, cfg->l_w, c) || !table_ok(cfg->lp_off, cfg->lp_w, c)) {
@@ -474,12 +478,25 @@ int sched_create(sched_t* out, const sched_config* cfg) {
       ClassParam& cp = h->base.cls[c];
       (which ? cp.lp_off : cp.l_off) = (uint32_t)thr_all.size();
       (which ? cp.lp_n : cp.l_n) = (uint32_t)t.size();
+      const size_t off0 = thr_all.size();
       for (size_t i = 0; i < t.size(); ++i) {
         cum += t[i].second;
         uint64_t th = (uint64_t)((cum << 32) / W);
         if (i + 1 == t.size()) th = (uint64_t)1 << 32;
         thr_all.push_back(th);
         val_all.push_back(t[i].first);
+      }
+      // guide table: guide[j] = min{i : j 2^(32-lg) < thr_i} (the answer for
+      // the lowest x of bucket j); the device scans forward from it
+      uint32_t lg = 1;
+      while (lg < 12 && ((size_t)1 << lg) < t.size()) ++lg;
+      (which ? cp.lp_goff : cp.l_goff) = (uint32_t)guide_all.size();
+      (which ? cp.lp_n : cp.l_n) |= lg << 24;
+      size_t i = 0;
+      for (uint64_t j = 0; j < ((uint64_t)1 << lg); ++j) {
+        const uint64_t x0 = j << (32 - lg);
+        while (thr_all[off0 + i] <= x0) ++i;
+        guide_all.push_back((uint16_t)i);
       }
     }
     h->base.cls[c].gap_scale = cfg->lambda[c] > 0 ? 1e12 / cfg->lambda[c] : 0.0;
@@ -561,6 +578,7 @@ int sched_create(sched_t* out, const sched_config* cfg) {
   p.b0 = cfg->tau_b0;
   h->h_cdf_thr = std::move(thr_all);
   h->h_cdf_val = std::move(val_all);
+  h->h_cdf_guide = std::move(guide_all);
   if (cfg->policy == SCHED_NESTED) {
     // stage -> segment index (bits 0-5, 63 = beyond the last segment) |
     // last stage of its segment << 6 | entry stage << 7 (reading R8)
@@ -791,6 +809,7 @@ void sched_destroy(sched_t h) {
   if (!h) return;
   cudaFree(h->d_cdf_thr);
   cudaFree(h->d_cdf_val);
+  cudaFree(h->d_cdf_guide);
   cudaFree(h->d_stage_info);
   cudaFree(h->d_ring_a);
   cudaFree(h->d_ring_e);

@@ -11,8 +11,9 @@ constexpr int kLanes = 32;
 
 struct ClassParam {
   double gap_scale;        // 1e12 / lambda (ticks per unit exponential); 0 = no arrivals
-  uint32_t l_off, l_n;     // CDF table slice (thresholds u64 [n-1], values u16 [n])
-  uint32_t lp_off, lp_n;
+  uint32_t l_off, l_n;     // CDF table slice (thresholds u64 [n], values u16 [n]);
+  uint32_t lp_off, lp_n;   // n in bits 0-23, guide-table log2 size in bits 24-27
+  uint32_t l_goff, lp_goff;  // guide-table slices (u16 [2^lg]) in cdf_guide
   uint32_t rf_off, rf_n;   // time-varying rate pieces (rf_n = 0: homogeneous)
 };
 
@@ -44,6 +45,7 @@ struct DevParams {
   ClassParam cls[kMaxClasses];
   const uint64_t* cdf_thr; // device
   const uint16_t* cdf_val; // device
+  const uint16_t* cdf_guide; // device: per table, guide[j] = first index whose threshold exceeds j 2^(32-lg)
   const uint8_t* stage_info; // NESTED: stage -> segment | entry<<7 (device)
   // time-varying classes: per piece start tick, integrated
   // rate at the start (operational ticks, 2^-32 expected arrivals), tick

@@ -82,17 +82,18 @@ __device__ __forceinline__ double neglog_bits(uint32_t x0, uint32_t x1) {
   return -lnU;
 }
 
-// inverse-CDF of an integer-weight table: idx = min{i : x < thr_i}
+// inverse-CDF of an integer-weight table: idx = min{i : x < thr_i}.  A guide
+// table (Chen & Asau) gives the answer for the lowest x of x's bucket, the
+// forward scan from it the exact same index as a binary search (usually 0-1
+// steps instead of log2 n dependent loads).
 __device__ __forceinline__ uint32_t cdf_sample(const uint64_t* __restrict__ thr,
-                                               const uint16_t* __restrict__ val, uint32_t off,
-                                               uint32_t n, uint32_t x) {
-  if (n == 1) return __ldg(val + off);
-  uint32_t lo = 0, hi = n - 1;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (__ldg(thr + off + mid) > (uint64_t)x) hi = mid; else lo = mid + 1;
-  }
-  return __ldg(val + off + lo);
+                                               const uint16_t* __restrict__ val,
+                                               const uint16_t* __restrict__ guide, uint32_t off,
+                                               uint32_t nlg, uint32_t goff, uint32_t x) {
+  if ((nlg & 0xFFFFFFu) == 1) return __ldg(val + off);
+  uint32_t i = __ldg(guide + goff + (x >> (32 - (nlg >> 24))));
+  while (__ldg(thr + off + i) <= (uint64_t)x) ++i;
+  return __ldg(val + off + i);
 }
 
 __device__ __forceinline__ int64_t warp_incl_scan_i64(int64_t x, int lane) {
@@ -207,7 +208,9 @@ __device__ __forceinline__ int64_t tv_tick_at(const int64_t* rf_B, const int64_t
 __device__ __forceinline__ void gen_window_impl(int lane, uint32_t base, int64_t prev, uint32_t rglob,
                                         uint32_t c, uint64_t seed, double gs,
                                         const uint64_t* __restrict__ cdf_thr,
-                                        const uint16_t* __restrict__ cdf_val, uint32_t l_off,
+                                        const uint16_t* __restrict__ cdf_val,
+                                        const uint16_t* __restrict__ cdf_guide, uint32_t l_goff,
+                                        uint32_t lp_goff, uint32_t l_off,
                                         uint32_t l_n, uint32_t lp_off, uint32_t lp_n,
                                         uint32_t rf_off, uint32_t rf_n, const int64_t* rf_B,
                                         const int64_t* rf_Lam, const double* rf_scale,
@@ -226,8 +229,8 @@ __device__ __forceinline__ void gen_window_impl(int lane, uint32_t base, int64_t
     } else {
       t = prev + warp_incl_scan_i64(__double2ll_rz(__dmul_rn(E, gs)), lane);
     }
-    l = cdf_sample(cdf_thr, cdf_val, l_off, l_n, x2);
-    lp = cdf_sample(cdf_thr, cdf_val, lp_off, lp_n, x3);
+    l = cdf_sample(cdf_thr, cdf_val, cdf_guide, l_off, l_n, l_goff, x2);
+    lp = cdf_sample(cdf_thr, cdf_val, cdf_guide, lp_off, lp_n, lp_goff, x3);
   }
   __syncwarp();
   wt[lane] = t;
@@ -239,12 +242,14 @@ __device__ __forceinline__ void gen_window_impl(int lane, uint32_t base, int64_t
 
 #define GEN_WINDOW_ARGS                                                                      \
   int lane, uint32_t base, int64_t prev, uint32_t rglob, uint32_t c, uint64_t seed, double gs, \
-      const uint64_t *cdf_thr, const uint16_t *cdf_val, uint32_t l_off, uint32_t l_n,         \
+      const uint64_t *cdf_thr, const uint16_t *cdf_val, const uint16_t *cdf_guide,            \
+      uint32_t l_goff, uint32_t lp_goff, uint32_t l_off, uint32_t l_n,                        \
       uint32_t lp_off, uint32_t lp_n, uint32_t rf_off, uint32_t rf_n, const int64_t *rf_B,    \
       const int64_t *rf_Lam, const double *rf_scale, int64_t *wt, uint16_t *wl, uint16_t *wlp, \
       int64_t *wtau
 #define GEN_WINDOW_PASS                                                                   \
-  lane, base, prev, rglob, c, seed, gs, cdf_thr, cdf_val, l_off, l_n, lp_off, lp_n, rf_off, \
+  lane, base, prev, rglob, c, seed, gs, cdf_thr, cdf_val, cdf_guide, l_goff, lp_goff, l_off, \
+      l_n, lp_off, lp_n, rf_off,                                                            \
       rf_n, rf_B, rf_Lam, rf_scale, wt, wl, wlp, wtau
 // one out-of-line copy (large kernels: instruction-cache footprint) ...
 __device__ __noinline__ void gen_window_call(GEN_WINDOW_ARGS) { gen_window_impl(GEN_WINDOW_PASS); }
@@ -385,7 +390,7 @@ struct WarpSim {
     }
     const ClassParam& cp = P.cls[c];
     gen_window<POL == SCHED_WAIT>(lane, base, prev, rglob, (uint32_t)c, P.seed, cp.gap_scale, P.cdf_thr, P.cdf_val,
-               cp.l_off, cp.l_n, cp.lp_off, cp.lp_n, cp.rf_off, cp.rf_n, P.rf_B, P.rf_Lam,
+               P.cdf_guide, cp.l_goff, cp.lp_goff, cp.l_off, cp.l_n, cp.lp_off, cp.lp_n, cp.rf_off, cp.rf_n, P.rf_B, P.rf_Lam,
                P.rf_scale, wt + c * 32, wl + c * 32, wlp + c * 32, wtau ? wtau + c * 32 : nullptr);
   }
 
@@ -474,7 +479,7 @@ struct WarpSim {
   // arrival every window still holds (an earlier epoch; ingest refills).
   __device__ int64_t idle_jump() const {
     int64_t bound = lane < P.K ? vt[lane * 32 + 31] : TMAX;
-    if (POL == SCHED_WAIT) {
+    if (POL == SCHED_WAIT || P.K == 1) {  // per FIFO: the (n - q)-th next arrival of its class
       int64_t cand = TMAX;
       if (lane < P.K) {
         const uint32_t q = k_vis - k_adm + (rtail - rhead);  // < n_j (type not qualifying)
