@@ -759,8 +759,14 @@ struct WarpSim {
             const size_t e = ring_slot(q, h0 + pos);
             a = P.ring_a[e];
             const uint32_t llp = P.ring_llp[e];
-            l = llp & 0xFFFFu; lp = (llp >> 16) & 0x7FFFu;
-            meta = (POL == SCHED_WAIT ? (uint32_t)q : 0u) | ((llp >> 31) ? META_FT : 0u) | META_RESTART;
+            uint32_t cls = POL == SCHED_WAIT ? (uint32_t)q : 0u;
+            if (RING) {  // {class, ft}: the class fixes l, l'
+              cls = llp & 0xFFu;
+              l = P.fl[cls] & 0xFFFFu; lp = P.fl[cls] >> 16;
+            } else {
+              l = llp & 0xFFFFu; lp = (llp >> 16) & 0x7FFFu;
+            }
+            meta = cls | ((llp >> 31) ? META_FT : 0u) | META_RESTART;
           }
         }
         for (int c = c_lo; c < c_hi; ++c) {
@@ -1068,7 +1074,8 @@ struct WarpSim {
         const size_t ri = ring_slot(q, tail_q + before);
         P.ring_a[ri] = e.a;
         P.ring_e[ri] = now;
-        P.ring_llp[ri] = l | (lp << 16) | (((xf & XF_FT) && !pend) ? 0x80000000u : 0u);
+        // ring engine: lengths are the class's, so the record keeps the class
+        P.ring_llp[ri] = v | (((xf & XF_FT) && !pend) ? 0x80000000u : 0u);
         sh_add_u32(&cnt[v], 1u);
         sh_add_u64(&xs[v], (uint64_t)x);
         if (pend) { sh_add_u32(&cnt[32 + v], ~0u); sh_add_u64(&psum()[v], (uint64_t)(-e.a)); }

@@ -309,7 +309,8 @@ def test_degenerate_horizons_and_capacity():
 # ------------------------------------------- both engines, every eligible case
 @pytest.mark.parametrize("engine", ["member", "ring"])
 @pytest.mark.parametrize("case", ["c2_wait", "c2_fcfs", "c2_ongoing", "c4_wait_evict", "c4_fcfs_evict",
-                                  "c1_wait_evict", "random_wait", "random_fcfs"])
+                                  "c1_wait_evict", "random_wait", "random_fcfs", "fcfs_evict_2cls",
+                                  "ongoing_evict_2cls"])
 def test_engines_bit_exact(engine, case, monkeypatch):
     """The member engine and the class-ring engine are two
     layouts of one semantics: forced either way, every row matches the
@@ -325,6 +326,13 @@ def test_engines_bit_exact(engine, case, monkeypatch):
         wl, pol, thr, n, T = W.c4(3), W.Policy(W.WAIT), [9, 6, 3], 12, 8.0
     elif case == "c4_fcfs_evict":
         wl, pol, thr, n, T = W.c4(4), W.Policy(W.FCFS, B=1024), [0], 12, 8.0
+    elif case in ("fcfs_evict_2cls", "ongoing_evict_2cls"):
+        # two fixed-length classes, tight M: FCFS evicts (LIFO) across classes,
+        # restarts must re-enter their own class ring
+        wl = W.Workload("ev2", [30.0, 40.0], [W.fixed(2), W.fixed(1)], [W.fixed(3), W.fixed(5)], M=20,
+                        horizon_s=3.0, seed=3, d0_s=0.02, d1_s=0.002)
+        kind = W.FCFS if case == "fcfs_evict_2cls" else W.FCFS_ONGOING
+        pol, thr, n, T = W.Policy(kind, B=1000), [0], 32, 3.0
     elif case == "c1_wait_evict":
         wl, pol, thr, n, T = W.C1, W.Policy(W.WAIT), [1], 32, W.C1.horizon_s
     else:
