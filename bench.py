@@ -34,6 +34,7 @@ UNIT = "request-steps/s"
 OPS_PER_REQUEST_STEP = 8
 OPS_PER_ARRIVAL = 400
 OPS_PER_BATCH = 100
+OPS_PER_EVICTION = 60   # LIFO victim (freed-KV scan share), restart record, FIFO re-rank
 
 
 def registry(name: str):
@@ -354,7 +355,8 @@ def main():
     clocks.start()
     t_step, t_kern = [], {n: [] for n, _, _ in scheds}
     tot_int = None
-    units = {n: {"request_steps": 0, "arrivals": 0, "batches": 0, "completed": 0} for n, _, _ in scheds}
+    units = {n: {"request_steps": 0, "arrivals": 0, "batches": 0, "completed": 0, "evictions": 0}
+             for n, _, _ in scheds}
     for k in range(args.steps):
         flush.zero_()
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -424,7 +426,7 @@ def main():
         solo.append((a.elapsed_time(b) / 1e3, {u: int(rows[dom][F_[u]].sum().item()) for u in units[dom]}))
     dur, u = solo[-1]
     ops_per_launch = (OPS_PER_REQUEST_STEP * u["request_steps"] + OPS_PER_ARRIVAL * u["arrivals"]
-                      + OPS_PER_BATCH * u["batches"])
+                      + OPS_PER_BATCH * u["batches"] + OPS_PER_EVICTION * u["evictions"])
     props = torch.cuda.get_device_properties(dev)
     sm_max, peak_src = 1965.0, "B200_PROFILING.md nominal clocks.max.sm (fallback)"
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -456,7 +458,8 @@ def main():
         "roofline": {"bound": "alu", "kernel": f"sim_kernel<{dom}>", "achieved": achieved,
                      "peak": peak_ops, "unit": "Tops/s", "frac": achieved / peak_ops, "traffic": traffic,
                      "ops_model": f"{OPS_PER_REQUEST_STEP}/request-step + {OPS_PER_ARRIVAL}/arrival "
-                                  f"+ {OPS_PER_BATCH}/batch (integer lane-ops, DESIGN.md §5.4)",
+                                  f"+ {OPS_PER_BATCH}/batch + {OPS_PER_EVICTION}/eviction (integer lane-ops, "
+                                  f"DESIGN.md §5.4)",
                      "peak_basis": f"{props.multi_processor_count} SMs x 4 warp-instr/clk x 32 lanes x "
                                    f"{sm_max:.0f} MHz ({peak_src})"},
         "kernel_ms": {n: 1e3 * sum(v) / len(v) for n, v in t_kern.items()},
