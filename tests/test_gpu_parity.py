@@ -381,3 +381,19 @@ def test_idle_skip_partial_jumps():
     check(wl, W.Policy(W.WAIT), [1, 2, 3], 16)
     check(wl, W.Policy(W.NESTED, seg_end=[2, 9]), [45, 20], 16)
     check(wl, W.Policy(W.NESTED, seg_end=[2, 9]), [3, 2], 16)
+
+
+def test_engine_selection_rule(monkeypatch):
+    """class-ring engine for fixed-length WAIT / short-decode
+    FCFS unless its footprint exceeds the member engine's by > 30%; Nested
+    and marks always use the member engine."""
+    from paper_2504_11320_b200 import Scheduler
+    monkeypatch.delenv("WAITSIM_ENGINE", raising=False)
+    eng = lambda wl, pol, thr=None: Scheduler(wl, pol, thr).launch_info()["engine"]
+    assert eng(W.C2, W.Policy(W.WAIT), [16, 16]) == 1
+    assert eng(W.C2, W.Policy(W.FCFS, B=1024)) == 1
+    assert eng(W.C3A, W.Policy(W.NESTED, seg_end=SEG3A), [7, 7, 7, 5]) == 0
+    assert eng(W.C3B, W.Policy(W.FCFS, B=2048)) == 0                 # marks
+    assert eng(W.c4(1), W.Policy(W.FCFS, B=1024)) == 0               # long decodes
+    assert eng(W.c4(4), W.Policy(W.WAIT), [18, 12, 6]) == 0          # rings 6,036 records vs 4,096
+    assert eng(W.c4(2), W.Policy(W.WAIT), [6, 4, 2]) == 1
