@@ -416,7 +416,15 @@ struct WarpSim {
   // INGEST (DESIGN.md §4.4 step 1): arrivals with t <= now and t < T become
   // visible (join their FIFO).  Cursor only: count + arrival-time sum.
   __device__ void ingest() {
-    for (int c = 0; c < P.K; ++c) {
+    // only classes whose next window entry is due (lane c: entry k_vis; the
+    // window always holds it, it is refilled before k_vis reaches its end)
+    bool due = false;
+    if (lane < P.K) {
+      const int64_t t = vt[lane * 32 + (k_vis - vbase)];
+      due = t <= now && t < P.T_t;
+    }
+    for (uint32_t todo = __ballot_sync(FULL, due); todo; todo &= todo - 1) {
+      const int c = __ffs(todo) - 1;
       for (;;) {
         uint32_t kv = kvis(c), vb = bcast32(vbase, c);
         if (kv == vb + 32) {
