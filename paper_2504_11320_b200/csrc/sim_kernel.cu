@@ -418,8 +418,9 @@ struct WarpSim {
   __device__ void ingest() {
     // only classes whose next window entry is due (lane c: entry k_vis; the
     // window always holds it, it is refilled before k_vis reaches its end)
-    bool due = false;
-    if (lane < P.K) {
+    // (with one or two classes both are usually due: skip the test)
+    bool due = lane < P.K;
+    if (P.K > 2 && due) {
       const int64_t t = vt[lane * 32 + (k_vis - vbase)];
       due = t <= now && t < P.T_t;
     }
