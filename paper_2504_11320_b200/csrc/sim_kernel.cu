@@ -4,13 +4,23 @@
 // counter.  Semantics: DESIGN.md §4 (event loop, policies, metrics), which
 // restates the paper passages cited inline.
 //
-// Layout per warp (shared memory, carved from dynamic smem):
-//   residents SoA in admission order: a[Rc] i64 (arrival tick), l[Rc],
-//     lp[Rc], s[Rc] (next stage to run), meta[Rc] (class | first-token<<8)
-//   per class: visibility window t[32], admission window t/l/lp[32]
-//   counters[64] (WAIT: residents per class; NESTED: [k] non-entry residents
-//     of segment k, [32+k] residents waiting at the entry stage of k),
-//   rank[32] (NESTED per-segment rank cursors).
+// Two resident engines, one semantics:
+//   member engine (template RING = false; every policy, length marks,
+//     explicit traces): residents in admission order as 16-byte records
+//     {a = arrival tick, l | l' << 16 | s << 32 | meta << 48}; a batch is one
+//     pass over them with ballot/popc compaction;
+//   class-ring engine (RING = true; WAIT / FCFS with fixed per-class
+//     lengths): residents of class c in their own ring, stage = class clock
+//     - admission clock, so a batch touches only completions and admissions.
+// Layout per warp (shared memory, carved from dynamic smem; warp_smem_bytes):
+//   residents (member) or staged admissions + 32 victim slots + class rings
+//   (RING); per class a generated window and a private admission window
+//   (t / l / l' of 32 arrivals each, one offset space); 32 staged restart
+//   ticks; counters[64] (WAIT: residents per class; NESTED: [k] non-entry
+//   residents of segment k, [32+k] residents waiting at its entry stage;
+//   RING: [32+c] pending first tokens), rank[32] / snap[32] (NESTED rank
+//   cursors; RING: pending first-token tick sums), WarpStats, RING eviction
+//   scratch, time-varying operational-time windows.
 // Per-class cursor state lives in REGISTERS of lane c (broadcast by shfl).
 // Waiting prompts hold no KV: new arrivals are cursor ranges
 // [k_adm, k_vis) of the class's Philox stream, regenerated at admission;
@@ -266,7 +276,7 @@ struct WarpSim {
   const int lane;
   // shared-memory views (this warp's slice)
   Rec* rr;                           // [Rc] residents in admission order (RING: staged admissions)
-  RRec* rg;                          // RING: class rings (ring c at P.roff[c], P.rcap[c] records)
+  RRec* rg;                          // RING: class rings (ring c: P.rcap[c] records from P.roff[c])
   int64_t* vt;                       // [K][32] generated window (t): visibility + admission
   uint16_t* vl; uint16_t* vlp;       // [K][32] generated window (l, l')
   int64_t* at;                       // [K][32] private admission windows (t)
