@@ -316,7 +316,8 @@ int prepare(sched_s* h) {
         L.rcap[c] = std::min<uint32_t>(L.rcap_safe[c], (uint32_t)(1.2 * tot * share) + 48);
         adm += h->n_star_c[c] / (double)(in.lp[c][0].first + 1);
       }
-      L.Rc = std::min<uint32_t>(L.Rc_safe, round32((uint64_t)(1.5 * adm) + 64));
+      // admissions per batch ~ Poisson(adm): mean + 8 sd + 16 (tail < 1e-12)
+      L.Rc = std::min<uint32_t>(L.Rc_safe, round32((uint64_t)(adm + 8.0 * std::sqrt(adm)) + 16));
     }
     if (int rc = size_cfg(L)) return rc;
     // the ring engine does O(classes + events) work per batch but its
