@@ -23,6 +23,7 @@ using namespace waitsim;
 struct LaunchCfg {
   bool ring = false;
   uint32_t Rc = 0, Rc_safe = 0;              // member: residents; ring: staging slots
+  uint32_t spare = 0;                        // ring: victim slots beyond Rc (8, 32 when evictions are expected)
   uint32_t rcap[32] = {}, rcap_safe[32] = {};  // ring: per-class ring capacity
   uint32_t warp_smem = 0, fb_warp_smem = 0;
   int grid = 0, block = 0, wpb = 0, blocks_per_sm = 0;
@@ -241,8 +242,8 @@ int prepare(sched_s* h) {
   auto size_cfg = [&](LaunchCfg& L) -> int {
     uint32_t rec = L.Rc, rec_safe = L.Rc_safe;
     if (L.ring) {
-      rec += 32;  // eviction-round victim slots
-      rec_safe += 32;
+      rec += L.spare;  // spare staging slots: eviction-round victims
+      rec_safe += L.spare;
       for (int c = 0; c < K; ++c) { rec += L.rcap[c]; rec_safe += L.rcap_safe[c]; }
     }
     L.fallback = rec < rec_safe;
@@ -319,13 +320,24 @@ int prepare(sched_s* h) {
       // admissions per batch ~ Poisson(adm): mean + 8 sd + 16 (tail < 1e-12)
       L.Rc = std::min<uint32_t>(L.Rc_safe, round32((uint64_t)(adm + 8.0 * std::sqrt(adm)) + 16));
     }
+    // victim slots per eviction round: 32 when memory binds (WAIT: M^pi > M,
+    // FCFS: M* > M), else 8 (evictions rare: save the shared memory)
+    {
+      double mpi = 0;
+      for (int c = 0; c < K && in.policy == SCHED_WAIT; ++c) {
+        const double l = in.l[c][0].first, lp = in.lp[c][0].first;
+        mpi += in.thresholds[c] * (lp * l + lp * (lp + 1) / 2);
+      }
+      const bool binds = in.policy == SCHED_WAIT ? mpi > (double)in.M : h->m_star > (double)in.M;
+      L.spare = binds ? 32u : 8u;
+    }
     if (int rc = size_cfg(L)) return rc;
     // the ring engine does O(classes + events) work per batch but its
     // per-class capacities can cost occupancy: keep it unless its
     // speculative footprint exceeds the member engine's by > 30%
     // (measured: C2, C4 rho=0.5/0.8 WAIT and C2 FCFS gain; C4 rho=0.95 WAIT
     // and long-l' FCFS lose)
-    uint64_t ring_rec = L.Rc + 32;
+    uint64_t ring_rec = L.Rc + L.spare;
     for (int c = 0; c < K; ++c) ring_rec += L.rcap[c];
     // FCFS additionally only for short decodes: with l' >> 1 most of an FCFS
     // batch is the fixed per-batch control both engines share and the ring
@@ -369,6 +381,7 @@ int prepare(sched_s* h) {
 // capacities of one launch of configuration L (safe = the fallback launch)
 void set_caps(DevParams& p, const LaunchCfg& L, bool safe, int K) {
   p.ring_engine = L.ring ? 1u : 0u;
+  p.spare = L.spare;
   p.Rc = safe ? L.Rc_safe : L.Rc;
   p.warp_smem = safe ? L.fb_warp_smem : L.warp_smem;
   uint32_t off = 0;

@@ -33,6 +33,7 @@ struct DevParams {
   // = class clock - admission clock, so a batch touches only the members
   // that complete, emit a first token or are admitted
   uint32_t ring_engine;
+  uint32_t spare;                  // staging slots beyond Rc for eviction-round victims (8 or 32)
   uint32_t rcap[kMaxClasses];      // ring capacity (records) of class c
   uint32_t roff[kMaxClasses];      // first record of ring c after the staging area
   uint32_t fl[kMaxClasses];        // fixed l | l' << 16 of class c

@@ -13,7 +13,7 @@
 //     lengths): residents of class c in their own ring, stage = class clock
 //     - admission clock, so a batch touches only completions and admissions.
 // Layout per warp (shared memory, carved from dynamic smem; warp_smem_bytes):
-//   residents (member) or staged admissions + 32 victim slots + class rings
+//   residents (member) or staged admissions + spare victim slots + class rings
 //   (RING); per class a generated window and a private admission window
 //   (t / l / l' of 32 arrivals each, one offset space); 32 staged restart
 //   ticks; counters[64] (WAIT: residents per class; NESTED: [k] non-entry
@@ -329,8 +329,8 @@ struct WarpSim {
     const uint32_t Rc = p.Rc;
     rr = (Rec*)base;
     // RING: 32 spare staging slots hold the victims of one eviction round
-    rg = (RRec*)(rr + Rc + (RING ? 32u : 0u));
-    vt = (int64_t*)(rr + Rc + (RING ? 32u + p.roff[p.K - 1] + p.rcap[p.K - 1] : 0u));
+    rg = (RRec*)(rr + Rc + (RING ? p.spare : 0u));
+    vt = (int64_t*)(rr + Rc + (RING ? p.spare + p.roff[p.K - 1] + p.rcap[p.K - 1] : 0u));
     at = vt + p.K * 32;
     re = at + p.K * 32;
     // l / l' of both windows share one offset space with the ticks:
@@ -1096,8 +1096,11 @@ struct WarpSim {
     if (peak <= P.M) return;
     int64_t excess = peak - P.M;
     const int K = P.K;
+    // victims of a round are staged after the admissions: up to 32, at least
+    // the P.spare slots beyond the staging capacity
+    const uint32_t vcap = min(32u, P.Rc + P.spare - n_new);
     while (excess > 0 && n_res > 0) {
-      const uint32_t nc = lane < K ? min(r_n, 32u) : 0u;  // class `lane`'s tail window
+      const uint32_t nc = lane < K ? min(r_n, vcap) : 0u;  // class `lane`'s tail window
       const uint32_t incl = warp_incl_scan_u32(nc, lane);
       const uint32_t ncand = __shfl_sync(FULL, incl, 31);
       const uint32_t my_off = lane < K ? P.roff[lane] : 0u, my_cap = lane < K ? P.rcap[lane] : 1u;
@@ -1128,11 +1131,11 @@ struct WarpSim {
           r += lo;
         }
         __syncwarp();
-        if (act && r < 32) { rr[sbase() + n_new + r] = Rec{e.a, (uint64_t)e.xf | ((uint64_t)sc << 32)}; }
+        if (act && r < vcap) { rr[sbase() + n_new + r] = Rec{e.a, (uint64_t)e.xf | ((uint64_t)sc << 32)}; }
         __syncwarp();
       }
       // (2) victims in LIFO order: lane r holds the r-th newest resident
-      const uint32_t nv = min(ncand, 32u);
+      const uint32_t nv = min(ncand, vcap);
       const bool valid = (uint32_t)lane < nv;
       Rec e = {0, 0};
       if (valid) e = rr[sbase() + n_new + lane];
