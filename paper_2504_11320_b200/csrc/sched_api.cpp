@@ -83,6 +83,7 @@ struct sched_s {
   bool use_ring = false;                     // sched_run uses the class-ring engine
   double n_star_c[32] = {};                  // fluid prompts in service per class
   double m_star = 0;                         // fluid KV occupancy M*
+  double tv_peak = 1.0;                      // max time-varying rate / lambda (speculative sizing)
   uint32_t* d_retry = nullptr;
   size_t retry_cap = 0;
   double n_star_total = 0;  // fluid equilibrium prompts in service (0 = unknown)
@@ -106,7 +107,9 @@ uint32_t speculative_rc(const sched_s* h, uint32_t safe) {
   uint64_t rc = safe;
   if (is_fcfs(in.policy)) {
     // FCFS residents ~ fluid prompts in service n* + margin
-    if (h->n_star_total > 0) rc = (uint64_t)(1.25 * h->n_star_total) + 64;
+    // (time-varying rates: the stationary fluid estimate does not hold and
+    // backlogs of the peak pieces fill B -- no speculation)
+    if (h->n_star_total > 0 && h->tv_peak <= 1.0) rc = (uint64_t)(1.25 * h->n_star_total) + 64;
   } else if (in.policy == SCHED_NESTED) {
     // non-entry stages hold <= n_k each; entry queues stay near n_k (Lemma,
     // PAPER.md:2345-2373) -- margin 2 n_k per boundary
@@ -310,12 +313,12 @@ int prepare(sched_s* h) {
       // by M / M* when memory binds and by B / n* when the batch cap binds
       // (WAIT needs no speculation: n_c per stage exactly, P14)
       const double fm = h->m_star > 0 ? std::min(1.0, (double)in.M / h->m_star) : 1.0;
-      const double tot = std::min((double)in.B, fm * h->n_star_total);
+      const double tot = std::min((double)in.B, fm * h->n_star_total * h->tv_peak);
       double adm = 0;
       for (int c = 0; c < K; ++c) {
         const double share = h->n_star_c[c] / h->n_star_total;
         L.rcap[c] = std::min<uint32_t>(L.rcap_safe[c], (uint32_t)(1.2 * tot * share) + 48);
-        adm += h->n_star_c[c] / (double)(in.lp[c][0].first + 1);
+        adm += h->tv_peak * h->n_star_c[c] / (double)(in.lp[c][0].first + 1);
       }
       // admissions per batch ~ Poisson(adm): mean + 8 sd + 16 (tail < 1e-12)
       L.Rc = std::min<uint32_t>(L.Rc_safe, round32((uint64_t)(adm + 8.0 * std::sqrt(adm)) + 16));
@@ -542,6 +545,8 @@ int sched_create(sched_t* out, const sched_config* cfg) {
         h->h_rf_Lam.push_back(Lam);
         h->h_rf_scale.push_back(r > 0 ? 1e12 / (r * 4294967296.0) : 0.0);
         pieces.push_back({cfg->rf_t[i], r});
+        // peak load relative to the constant rate the fluid setup uses
+        if (cfg->lambda[c] > 0) h->tv_peak = std::max(h->tv_peak, r / cfg->lambda[c]);
       }
       h->tv_any = true;
     }

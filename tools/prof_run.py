@@ -19,6 +19,9 @@ elif wl_name.startswith("C4_"):
     pols = [W.Policy(W.WAIT), W.Policy(W.NESTED, seg_end=[100, 200, 300]), W.Policy(W.FCFS, B=1024)]
 elif wl_name == "C3a":
     wl, pols = W.C3A, [W.Policy(W.NESTED, seg_end=[20, 40, 80, 160]), W.Policy(W.FCFS, B=1024)]
+elif wl_name == "C3a_tv":
+    wl, pols = W.c3a_time_varying(), [W.Policy(W.NESTED, seg_end=[20, 40, 80, 160], thresholds=[11, 11, 10, 7]),
+                                      W.Policy(W.FCFS, B=1024)]
 elif wl_name == "C3b":
     wl, pols = W.C3B, [W.Policy(W.NESTED, seg_end=seg10), W.Policy(W.FCFS, B=2048)]
 else:
