@@ -139,8 +139,23 @@ uint32_t speculative_rc(const sched_s* h, uint32_t safe) {
       num += in.lambda[c] * (ep1 * el + eq);
       den += in.lambda[c] * ep1;
     }
+    // when memory binds (M^pi = sum_k n_k sum_{s in seg k} (E[l] + s) > M,
+    // reading R9) LIFO eviction keeps young, small residents: wider margin
+    double el = 0, lam = 0, mpi = 0;
+    for (size_t c = 0; c < in.lambda.size(); ++c) {
+      double w = 0, e = 0;
+      for (auto& t : in.l[c]) { w += (double)t.second; e += (double)t.second * t.first; }
+      if (w > 0) { el += in.lambda[c] * e / w; lam += in.lambda[c]; }
+    }
+    el = lam > 0 ? el / lam : 1.0;
+    uint32_t prev = 0;
+    for (size_t k = 0; k < in.seg_end.size() && k < in.thresholds.size(); ++k) {
+      for (uint32_t st = (k ? prev + 1 : 0); st <= in.seg_end[k]; ++st) mpi += in.thresholds[k] * (el + st);
+      prev = in.seg_end[k];
+    }
+    const double factor = mpi > (double)in.M ? 2.0 : 1.4;
     if (num > 0 && den > 0)
-      rc = std::min<uint64_t>(rc, (uint64_t)(1.4 * (double)in.M / (num / den)) + 96);
+      rc = std::min<uint64_t>(rc, (uint64_t)(factor * (double)in.M / (num / den)) + 96);
   }
   return std::min(safe, round32(rc));
 }
