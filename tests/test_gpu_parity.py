@@ -397,3 +397,40 @@ def test_engine_selection_rule(monkeypatch):
     assert eng(W.c4(1), W.Policy(W.FCFS, B=1024)) == 0               # long decodes
     assert eng(W.c4(4), W.Policy(W.WAIT), [18, 12, 6]) == 0          # rings 6,036 records vs 4,096
     assert eng(W.c4(2), W.Policy(W.WAIT), [6, 4, 2]) == 1
+
+
+@pytest.mark.parametrize("name", ["C3a", "C3b", "C4", "C5"])
+def test_full_size_bench_workloads_sampled(name):
+    """Every bench workload at its bench launch configuration (bench.py's
+    registry: replication counts, horizons, thresholds from sched_thresholds,
+    handle options), sampled replications checked against the oracle one by
+    one, conservation and the memory bound checked on every row."""
+    import importlib.util
+    import os
+    from paper_2504_11320_b200 import Scheduler
+    from paper_2504_11320_b200.sim import run_rows
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    pols, reps, _ = bench.expand(name)
+    if name == "C4":
+        pols = [p for p in pols if p[0].endswith("@0.5") or p[0].endswith("@0.9")]
+    kw = bench.SCHED_KW.get(name, {})
+    n_check = 2 if name == "C5" else 4
+    for label, pol, thr, wl in pols:
+        s = Scheduler(wl, pol, thr, **kw)
+        if thr is None and pol.kind in (W.WAIT, W.NESTED):
+            thr = s.thresholds()["thresholds"]
+        rows = run_rows(s, wl.seed, 0, reps, wl.horizon_s)
+        torch.cuda.synchronize()
+        got = rows.cpu().numpy().view(np.uint64)
+        s.close()
+        assert (got[oracle.F["status"]] == 0).all(), label
+        for i in np.linspace(0, reps - 1, n_check).astype(int).tolist():
+            ref = oracle.run(wl, pol, thr if thr is not None else [0], n_reps=1, rep_begin=i)
+            assert_rows_equal(got[:, i:i + 1], ref, f"{name}/{label} rep {i}")
+        f = lambda k: got[oracle.F[k]].astype(object)
+        assert (f("arrivals") == f("completed") + f("completed_after_T") + f("final_waiting")
+                + f("final_resident")).all()
+        assert (got[oracle.F["max_kv_peak"]] <= wl.M).all()
