@@ -782,7 +782,9 @@ struct WarpSim {
           o1 = ka - ab;
           n1 = min(p, pc - o1);
           if (n1 < p && ab + pc == vb) n2 = min(p - n1, 32u - n1);
-          if (n1 + n2 < min(p, 32u)) {
+          // ranks < m <= min(want, 32) are exact when every source offers
+          // min(pending, want, 32) candidates
+          if (n1 + n2 < min(p, min(want, 32u))) {
             // backlog deeper than the windows: regenerate the private window
             const int64_t prev = carry_before(c, ka);
             fill<true>(c, ka, prev, at, al, alp);
