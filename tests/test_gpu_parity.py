@@ -434,3 +434,17 @@ def test_full_size_bench_workloads_sampled(name):
         assert (f("arrivals") == f("completed") + f("completed_after_T") + f("final_waiting")
                 + f("final_resident")).all()
         assert (got[oracle.F["max_kv_peak"]] <= wl.M).all()
+
+
+def test_r28_trace_log():
+    """Reading R28 (class-major simultaneous WAIT admissions decide the LIFO
+    victim), the hand-traced CPU pin's trace through sched_run_trace."""
+    from paper_2504_11320_b200 import Scheduler
+    from test_oracle import _r28_trace
+    wl, tr = _r28_trace()
+    ref_rows, ref_log = oracle.run_trace(wl, W.Policy(W.WAIT), [1, 1], [tr], log_cap=8)
+    s = Scheduler(wl, W.Policy(W.WAIT), [1, 1])
+    rows, log = s.run_trace([tr], wl.horizon_s, log_cap=8)
+    assert np.array_equal(log, ref_log)
+    assert_rows_equal(rows, ref_rows, "R28")
+    assert (int(log[1][2]), int(log[1][4])) == (5, 1)  # tokens, evictions of batch 2

@@ -241,6 +241,32 @@ def test_example2_fcfs_cascade():
     assert got[2][0] == 4 * 1 + 4 * 2
 
 
+def _r28_trace():
+    """Two WAIT types qualifying together, thresholds (1, 1):
+    type 0 (l=1, l'=3), type 1 (l=2, l'=3); both arrive at t=0 and t=1 s;
+    d0 = 1/2 s, d1 = 0; M = 6."""
+    wl = W.Workload("r28", [1.0, 1.0], [W.fixed(1), W.fixed(2)], [W.fixed(3), W.fixed(3)], M=6,
+                    horizon_s=3.0, seed=0, d0_s=0.5, d1_s=0.0)
+    tr = [(0, 0, 1, 3), (0, 1, 2, 3), (TPS, 0, 1, 3), (TPS, 1, 2, 3)]
+    return wl, tr
+
+
+def test_r28_class_major_admission_order_decides_the_lifo_victim():
+    """Reading R28 by hand: batch 1 admits type 0 then type 1 (class-major).
+    Batch 2 (t = 1 s): residents KV 1 + 2 = 3, plan = both residents (+1
+    each) + two new prefills (1 + 2): peak 3 + 2 + 3 = 8 > M = 6, so LIFO
+    evicts the last admitted -- the type-1 resident, freeing (2+1-1)+1 = 3 ->
+    peak 5; tokens = type-0 resident (1+1) + new (1+2) = 5.  (Type-major in
+    the other order would evict type 0 and run 6 tokens.)"""
+    wl, tr = _r28_trace()
+    rows, log = oracle.run_trace(wl, W.Policy(W.WAIT), [1, 1], [tr], log_cap=8)
+    got = [(int(r[1]), int(r[2]), int(r[3]), int(r[4]), int(r[5]), int(r[6])) for r in log]
+    # (|plan|, tokens, n_complete, n_evict, n_new, peak)
+    assert got[0] == (2, 3, 0, 0, 2, 3)
+    assert got[1] == (3, 5, 0, 1, 2, 5)
+    assert int(rows[F["evictions"], 0]) >= 1
+
+
 def test_example2_sarathi_ongoing_first():
     """FCFS ongoing-first (Sarathi; reading R29) on the same
     trace, by hand: b2 admits 6 (KV 3 + growth 3 + 6 <= 12); b3 admits none
