@@ -239,7 +239,7 @@ int prepare(sched_s* h) {
   }
   // choose warps per block maximising resident warps per SM
   auto size_launch = [&](bool ring, uint32_t records, uint32_t* wsm, int* wpb_out, int* bps_out) -> int {
-    *wsm = warp_smem_bytes(records, K, h->tv_any, ring);
+    *wsm = warp_smem_bytes(records, K, h->tv_any, ring, h->in.policy == SCHED_NESTED);
     int best_w = 0;
     const int cands[] = {8, 4, 2, 1};
     for (int wpb : cands) {

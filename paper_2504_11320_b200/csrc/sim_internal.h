@@ -79,7 +79,7 @@ struct DevParams {
 };
 
 // shared-memory bytes per warp for a given resident capacity / class count
-inline uint32_t warp_smem_bytes(uint32_t Rc, int K, bool tv = false, bool ring = false) {
+inline uint32_t warp_smem_bytes(uint32_t Rc, int K, bool tv = false, bool ring = false, bool nested = false) {
   uint32_t b = Rc * 16u;                    // residents: a (i64) + packed (l, l', s, meta)
   b += (uint32_t)K * (32u * 12u);           // generated windows (t, l, l')
   b += (uint32_t)K * (32u * 12u);           // private admission windows (t, l, l')
@@ -87,6 +87,7 @@ inline uint32_t warp_smem_bytes(uint32_t Rc, int K, bool tv = false, bool ring =
   b += (64u + 32u + 32u) * 4u + 16u;        // counters, rank cursors, snapshot, align
   b += 256u;                                // WarpStats (metric accumulators)
   if (ring) b += 256u;                      // class-ring eviction scratch
+  if (nested) b += ((Rc + 31u) / 32u + 15u) & ~15u;  // per-chunk activity summaries
   if (tv) b += (uint32_t)K * (32u * 16u);   // operational-time windows (generated, private)
   return (b + 15u) & ~15u;
 }

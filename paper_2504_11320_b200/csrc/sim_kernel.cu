@@ -288,6 +288,7 @@ struct WarpSim {
   uint32_t* snap;                    // [32] NESTED entry counts at decision time
   WarpStats* st;                     // metric accumulators
   uint64_t* xs;                      // [32] RING eviction scratch (per-class sums)
+  uint8_t* csum;                     // NESTED: per-chunk lowest resident segment
   size_t ring_base;                  // first ring entry of this warp slot
 
   // per-class cursor state, lane c holds class c (and ring c for WAIT; ring 0
@@ -344,7 +345,9 @@ struct WarpSim {
     snap = rank + 32;
     st = (WarpStats*)(snap + 32);
     xs = (uint64_t*)((unsigned char*)st + 256);
-    vtau = (int64_t*)((unsigned char*)st + (RING ? 512 : 256));
+    csum = (uint8_t*)st + (RING ? 512 : 256);  // NESTED: (Rc + 31) / 32 chunk summaries
+    vtau = (int64_t*)((unsigned char*)st + (RING ? 512 : 256) +
+                      (POL == SCHED_NESTED ? (((p.Rc + 31) / 32 + 15) & ~15u) : 0u));
     atau = vtau + p.K * 32;
   }
 
@@ -1200,6 +1203,7 @@ struct WarpSim {
   struct Upd {
     bool keep, inp;
     uint32_t l, lp, ns, meta;
+    uint32_t seg;  // NESTED: segment after the step (chunk activity summary)
   };
 
   // S5 per-member step: membership, first token, completion or s++
@@ -1237,6 +1241,7 @@ struct WarpSim {
     u.keep = valid;
     u.inp = inp;
     u.ns = s;
+    if (POL == SCHED_NESTED) u.seg = fresh ? 0u : info_seg(info_s);
     if (inp) {
       acc.tok += u.l + s;
       // the stage-1 iteration emits the first output token
@@ -1258,6 +1263,7 @@ struct WarpSim {
           // (-> the next segment's entry stage)
           const uint32_t seg = info_seg(info_s);
           const uint32_t key_n = (info_s & 0x40) ? 32u + seg + 1u : seg;
+          if (info_s & 0x40) u.seg = seg + 1;
           sh_add_u32(&cnt[key_s], ~0u);
           sh_add_u32(&cnt[key_n], 1u);
         }
@@ -1275,6 +1281,24 @@ struct WarpSim {
     const uint32_t d = wp + __popc(km & lanemask_lt());
     if (u.keep) rr[d] = Rec{a, pack_q(u.l, u.lp, u.ns, u.meta)};
     wp += __popc(km);
+  }
+
+  // Nested compaction + chunk activity summaries: csum[x] = the lowest
+  // segment of the residents in chunk x (slots 32x..32x+31); a chunk whose
+  // residents all sit in segments > k* takes no part in the batch and, while
+  // nothing before it moved, is skipped
+  __device__ __forceinline__ void compact_n(const Upd& u, int64_t a, uint32_t& wp) {
+    const uint32_t km = __ballot_sync(FULL, u.keep);
+    const uint32_t d = wp + __popc(km & lanemask_lt());
+    if (u.keep) rr[d] = Rec{a, pack_q(u.l, u.lp, u.ns, u.meta)};
+    const uint32_t c0 = wp >> 5, kept = __popc(km);
+    const uint32_t m0 = __reduce_min_sync(FULL, (u.keep && (d >> 5) == c0) ? u.seg : 0xFFu);
+    const uint32_t m1 = __reduce_min_sync(FULL, (u.keep && (d >> 5) != c0) ? u.seg : 0xFFu);
+    if (lane == 0 && kept) {
+      csum[c0] = (wp & 31u) ? (uint8_t)min((uint32_t)csum[c0], m0) : (uint8_t)m0;
+      if (((wp + kept - 1) >> 5) != c0) csum[c0 + 1] = (uint8_t)m1;
+    }
+    wp += kept;
   }
 
   // WAIT / FCFS per-member step + compaction, branch-light: membership,
@@ -1443,16 +1467,41 @@ struct WarpSim {
         if (base + 32 < n_tot) step_plain(i1, v1, e1, acc, wp);
       }
     } else {
-      for (uint32_t base = 0; base < n_tot; base += 64) {
-        const uint32_t i0 = base + lane, i1 = i0 + 32;
-        const bool v0 = i0 < n_tot, v1 = i1 < n_tot;
-        Rec e0 = {0, 0}, e1 = {0, 0};
-        if (v0) e0 = rr[i0];
-        if (v1) e1 = rr[i1];
-        const Upd u0 = member(v0, i0 >= n_res, e0.a, e0.q, over, acc);
-        const Upd u1 = member(v1, i1 >= n_res, e1.a, e1.q, over, acc);
-        compact(u0, e0.a, wp);
-        compact(u1, e1.a, wp);
+      // most residents idle (waiting at entry stages of inactive segments,
+      // e.g. the thrashing C5 regime): keep chunk summaries and skip idle
+      // chunks; otherwise plain passes, which mark what they wrote as active
+      if (n_plan_res * 4 < n_res) {
+        for (uint32_t base = 0; base < n_tot; base += 64) {
+          // two idle chunks with nothing moved before them: skip
+          if (wp == base && base + 64 <= n_res && csum[base >> 5] > (uint32_t)kstar &&
+              csum[(base >> 5) + 1] > (uint32_t)kstar) {
+            wp += 64;
+            continue;
+          }
+          const uint32_t i0 = base + lane, i1 = i0 + 32;
+          const bool v0 = i0 < n_tot, v1 = i1 < n_tot;
+          Rec e0 = {0, 0}, e1 = {0, 0};
+          if (v0) e0 = rr[i0];
+          if (v1) e1 = rr[i1];
+          const Upd u0 = member(v0, i0 >= n_res, e0.a, e0.q, over, acc);
+          const Upd u1 = member(v1, i1 >= n_res, e1.a, e1.q, over, acc);
+          compact_n(u0, e0.a, wp);
+          compact_n(u1, e1.a, wp);
+        }
+      } else {
+        for (uint32_t base = 0; base < n_tot; base += 64) {
+          const uint32_t i0 = base + lane, i1 = i0 + 32;
+          const bool v0 = i0 < n_tot, v1 = i1 < n_tot;
+          Rec e0 = {0, 0}, e1 = {0, 0};
+          if (v0) e0 = rr[i0];
+          if (v1) e1 = rr[i1];
+          const Upd u0 = member(v0, i0 >= n_res, e0.a, e0.q, over, acc);
+          const Upd u1 = member(v1, i1 >= n_res, e1.a, e1.q, over, acc);
+          compact(u0, e0.a, wp);
+          compact(u1, e1.a, wp);
+        }
+        __syncwarp();
+        for (uint32_t x = lane; x < (wp + 31) / 32; x += 32) csum[x] = 0;  // unknown: active
       }
     }
     __syncwarp();
