@@ -70,7 +70,8 @@ enum {
   SCHED_F_FINAL_WAITING,        /* prompts in FIFOs at stop */
   SCHED_F_FINAL_RESIDENT,       /* GPU-resident prompts at stop */
   SCHED_F_TRAJ_HASH,            /* 64-bit trajectory hash */
-  SCHED_F_STATUS,               /* 0 ok; 1 resident overflow; 2 restart overflow */
+  SCHED_F_STATUS,               /* 0 ok; 1 resident overflow; 2 restart overflow (the CPU
+                                   oracle also uses 3: invariant P14 violated) */
   SCHED_F_NOW_STOP,             /* simulated clock at stop */
   SCHED_F_SUM_WAITING,          /* sum over batches of waiting prompts at decision */
   SCHED_NF

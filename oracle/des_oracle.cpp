@@ -174,6 +174,7 @@ struct Setup {  // per-config constants, recomputed here from the raw config
   std::vector<uint32_t> thr;
   std::vector<int> seg_end;
   uint32_t B, tok_budget;
+  int max_stage = 0;               // largest decode length any table or trace can hold
   explicit Setup(const orc_config* cfg) {
     K = cfg->K; policy = cfg->policy;
     for (int c = 0; c < K; ++c) {
@@ -182,6 +183,7 @@ struct Setup {  // per-config constants, recomputed here from the raw config
       a.build(cfg->l_val + cfg->l_off[c], cfg->l_w + cfg->l_off[c], cfg->l_off[c + 1] - cfg->l_off[c]);
       b.build(cfg->lp_val + cfg->lp_off[c], cfg->lp_w + cfg->lp_off[c], cfg->lp_off[c + 1] - cfg->lp_off[c]);
       ltab.push_back(a); lptab.push_back(b);
+      for (uint16_t v : b.val) max_stage = std::max<int>(max_stage, v);
       RatePieces pc;
       if (cfg->rf_off && cfg->rf_off[c + 1] > cfg->rf_off[c])
         pc.build(cfg->rf_t + cfg->rf_off[c], cfg->rf_rate + cfg->rf_off[c], cfg->rf_off[c + 1] - cfg->rf_off[c]);
@@ -254,6 +256,10 @@ struct Sim {
   std::vector<ArrivalStream> streams;
   std::vector<std::deque<Prompt>> fifo;   // WAIT: one per class; else one
   std::vector<Prompt> res;                // GPU-resident, admission order
+  // per (row, stage) prompt counters of the decision step, row = class
+  // (WAIT) or 0 (NESTED: the stage fixes the segment); zeroed after use
+  std::vector<uint64_t> qcnt;
+  size_t qw = 0;
   int64_t now = 0, KV = 0;                // KV = sum over residents of (l+s-1)
   // metrics
   uint64_t arrivals = 0, admitted = 0, completed = 0, completed_after_T = 0,
@@ -267,6 +273,8 @@ struct Sim {
 
   Sim(const Setup& s, uint64_t seed_, uint32_t r_) : S(s), seed(seed_), r(r_) {
     fifo.resize(S.policy == ORC_WAIT ? S.K : 1);
+    qw = (size_t)std::max(S.max_stage, S.seg_end.empty() ? 0 : S.seg_end.back()) + 2;
+    qcnt.assign((S.policy == ORC_WAIT ? S.K : 1) * qw, 0);
     h = mix64(seed ^ ((uint64_t)r * 0x9E3779B97F4A7C15ull));
   }
   int fifo_of(int c) const { return S.policy == ORC_WAIT ? c : 0; }
@@ -308,11 +316,32 @@ struct Sim {
     return (int)S.seg_end.size();  // beyond the last segment (invalid config)
   }
 
+  // Invariant P14 (follows by induction from Alg. 1
+  // / Alg. 2 "Advance min{n_k, Q_{k,s}}"): WAIT stage counts Q_{j,s} <= n_j
+  // for s >= 1; Nested non-entry stages Q_{k,s} <= n_k.  Checked at every
+  // decision epoch; a violation marks the row with status 3 (never set by
+  // a correct simulator: the tests require status 0).
+  uint64_t& q_at(const Prompt& p) { return qcnt[(S.policy == ORC_WAIT ? p.c : 0) * qw + p.s]; }
+  void clear_q() { for (const Prompt& p : res) q_at(p) = 0; }
+  void check_p14() {
+    for (const Prompt& p : res) {
+      if (S.policy == ORC_WAIT) {
+        if (++q_at(p) > S.thr[p.c]) status = 3;
+      } else if (S.policy == ORC_NESTED) {
+        const int k = segment_of(p.s);
+        const bool entry = k >= 1 && p.s == S.seg_end[k - 1] + 1;
+        if (!entry && ++q_at(p) > S.thr[k]) status = 3;
+      }
+    }
+    clear_q();
+  }
+
   // DECIDE.  Returns false for "no batch: wait".
   bool decide(Plan& P) {
     P.res_in.assign(res.size(), 0);
     P.new_fifo.clear(); P.new_pos.clear();
     if (S.policy == ORC_WAIT) {
+      check_p14();
       // Algorithm 1 line "Check if n_j0 >= n_j": Q = classes
       // whose waiting inventory reached the threshold.
       std::vector<char> inQ(S.K, 0);
@@ -320,19 +349,27 @@ struct Sim {
       for (int c = 0; c < S.K; ++c)
         if (fifo[c].size() >= S.thr[c]) { inQ[c] = 1; any = true; }
       if (!any) return false;
-      // min{n_j, n_js} prompts of type j at each stage s for
-      // all j meeting the condition.  Stage counts of residents never exceed
-      // n_j (invariant P14), so every resident of a qualifying type is in.
-      for (size_t i = 0; i < res.size(); ++i) P.res_in[i] = inQ[res[i].c];
-      for (int c = 0; c < S.K; ++c)  // stage 0: the first n_j waiting prompts
+      // "selecting min{n_j, n_js} prompts of type j at each
+      // stage s for all j meeting the condition" -- the oldest (admission
+      // order) first at every stage s >= 1 (reading R6) ...
+      for (size_t i = 0; i < res.size(); ++i) {
+        const Prompt& p = res[i];
+        if (!inQ[p.c]) continue;  // line 1491: other types wait, KV kept
+        uint64_t& taken = q_at(p);  // selected so far at (type, stage)
+        if (taken < S.thr[p.c]) { P.res_in[i] = 1; ++taken; }
+      }
+      clear_q();
+      // ... and at stage 0 the first n_j waiting prompts, class-major (R28)
+      for (int c = 0; c < S.K; ++c)
         if (inQ[c])
           for (uint32_t j = 0; j < S.thr[c]; ++j) { P.new_fifo.push_back(c); P.new_pos.push_back((int)j); }
       return true;
     }
     if (S.policy == ORC_NESTED) {
+      check_p14();
       // Algorithm 2 line "Find largest k such that Q_{k', entry} >= n_k' for
       // all k' <= k".  Segment 1's entry stage is stage 0
-      // (the FIFO); segment k>=2 enters at stage e_{k-1}+1.
+      // (the FIFO); segment k>=2 enters at stage e_{k-1}+1 (reading R8).
       const int L = (int)S.seg_end.size();
       if (fifo[0].size() < S.thr[0]) return false;
       int kstar = 0;  // 0-based index of the last active segment
@@ -342,19 +379,18 @@ struct Sim {
         for (const Prompt& p : res) cnt += (p.s == entry);
         if (cnt >= S.thr[k]) kstar = k; else break;
       }
-      // select min{n_k', Q_{k',s}} per stage of segments
-      // 1..k*, oldest (admission order) first.
-      std::vector<uint64_t> taken(L, 0);
+      // "Form batch from segments 1, ..., k: select
+      // min{n_k', Q_{k',s}} prompts per stage", the oldest (admission order)
+      // first at every stage (reading R6); prompts of later segments wait
+      // with their KV (line 1643).
       for (size_t i = 0; i < res.size(); ++i) {
-        const int s = res[i].s;
-        const int k = segment_of(s);
+        const int k = segment_of(res[i].s);
         if (k > kstar) continue;
-        if (k >= 1 && s == S.seg_end[k - 1] + 1) {
-          if (taken[k] < S.thr[k]) { P.res_in[i] = 1; ++taken[k]; }
-        } else {
-          P.res_in[i] = 1;
-        }
+        uint64_t& taken = q_at(res[i]);  // selected so far at this stage
+        if (taken < S.thr[k]) { P.res_in[i] = 1; ++taken; }
       }
+      clear_q();
+      // stage 0 of segment 1: the first n_1 prompts of the FIFO
       for (uint32_t j = 0; j < S.thr[0]; ++j) { P.new_fifo.push_back(0); P.new_pos.push_back((int)j); }
       return true;
     }
@@ -396,7 +432,11 @@ struct Sim {
       bool go = decide(P);                        // step 3
       uint64_t n_evict = 0;
       int64_t peak = 0;
-      uint64_t waiting = 0;  // waiting prompts at decision time (before admission/eviction)
+      // waiting inventory the decision reads (n_j0 of Alg. 1 line 1488 /
+      // Q_{1,0} of Alg. 2): after ingest, before admission and
+      // before this epoch's evictions (reading R32; summed over executed
+      // batches, it is the pre-service queue of the Kingman bounds, P17)
+      uint64_t waiting = 0;
       for (auto& q : fifo) waiting += q.size();
       if (go) {
         // step 4, MEMORY: the KV held after this iteration must fit in M
@@ -592,6 +632,7 @@ int64_t orc_run_trace(const orc_config* cfg, const int64_t* t, const int32_t* cl
                       const int32_t* l, const int32_t* lp, const int64_t* off,
                       int64_t n_reps, uint64_t* out, int64_t* log, int64_t log_cap) {
   Setup S(cfg);
+  for (int64_t a = 0; a < off[n_reps]; ++a) S.max_stage = std::max<int>(S.max_stage, lp[a]);
   int64_t logged = 0;
   for (int64_t i = 0; i < n_reps; ++i) {
     Sim sim(S, 0, (uint32_t)i);

@@ -448,3 +448,31 @@ def test_r28_trace_log():
     assert np.array_equal(log, ref_log)
     assert_rows_equal(rows, ref_rows, "R28")
     assert (int(log[1][2]), int(log[1][4])) == (5, 1)  # tokens, evictions of batch 2
+
+
+# ---------------------------------------------- hand traces (tests/hand_traces.py)
+@pytest.mark.parametrize("case", ["nested_A", "nested_B", "fcfs_budget"])
+def test_hand_traces_replayed(case):
+    """The hand-derived batch logs and rows of the multi-segment Nested WAIT
+    traces (Alg. 2: k* prefix, >= at equality,
+    oldest-first entry stage, paused KV, LIFO cascade) and the FCFS token
+    budget, replayed through sched_run_trace: equal to the hand values and
+    to the oracle, element by element."""
+    import hand_traces as H
+    from paper_2504_11320_b200 import Scheduler
+    if case == "fcfs_budget":
+        wl, pol, thr, T, log_exp, row_exp = (H.fcfs_workload(), H.FCFS_POLICY, [0], 10.0, H.FCFS_LOG,
+                                             H.FCFS_ROW)
+        tr = H.FCFS_TRACE
+    else:
+        M, log_exp, row_exp = ((H.NESTED_A_M, H.NESTED_A_LOG, H.NESTED_A_ROW) if case == "nested_A"
+                               else (H.NESTED_B_M, H.NESTED_B_LOG, H.NESTED_B_ROW))
+        wl, pol, thr, T, tr = H.nested_workload(M), H.NESTED_POLICY, H.NESTED_THR, H.NESTED_T_S, H.NESTED_TRACE
+    s = Scheduler(wl, pol, thr if pol.kind != W.FCFS else None)
+    rows, log = s.run_trace([tr], T, log_cap=64)
+    s.close()
+    assert [tuple(int(x) for x in r) for r in log] == log_exp
+    assert H.row_matches(rows, 0, row_exp, oracle.F, oracle.u128) == {}
+    ref_rows, ref_log = oracle.run_trace(wl, pol, thr, [tr], log_cap=64, horizon_s=T)
+    assert np.array_equal(log, ref_log)
+    assert_rows_equal(rows, ref_rows, case)

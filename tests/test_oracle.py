@@ -59,13 +59,15 @@ def test_poisson_counts_and_gaps():
     """Arrival counts in [0,T) are Poisson(lambda T); gaps are Exp(lambda)."""
     wl = W.Workload("p", [50.0], [W.fixed(1)], [W.fixed(1)], M=100, horizon_s=20.0, seed=7)
     counts = []
-    for r in range(300):
-        t, _, _ = oracle.gen_arrivals(wl, r, 0, 2000)
+    for r in range(10_000):  # SURVEY P3: 10^4 replications, mean within 1%, variance within 5%
+        t, _, _ = oracle.gen_arrivals(wl, r, 0, 1300)
+        assert t[-1] >= 20 * TPS
         counts.append(int((t < 20 * TPS).sum()))
     counts = np.array(counts, dtype=float)
     mu = 50 * 20
+    assert abs(counts.mean() / mu - 1) < 0.01
     assert abs(counts.mean() - mu) < 4 * math.sqrt(mu / len(counts))
-    assert abs(counts.var(ddof=1) / mu - 1) < 0.25
+    assert abs(counts.var(ddof=1) / mu - 1) < 0.05
     t, _, _ = oracle.gen_arrivals(wl, 0, 0, 20000)
     gaps = np.diff(np.concatenate([[0], t])) / TPS
     # Kolmogorov-Smirnov against Exp(50)
@@ -316,7 +318,7 @@ def _wait_maxplus(a, n, l, lp, d0, d1, T):
         E.append(s + d0 + d1 * tok)
         b += 1
     nb = len(S)
-    done = lat = ttft = nft = after = 0
+    done = lat = ttft = nft = after = cbi = 0
     for c in range(1, nb + 1):
         coh = a[(c - 1) * n: c * n]
         if c + 1 <= nb and E[c + 1] <= T:
@@ -326,10 +328,15 @@ def _wait_maxplus(a, n, l, lp, d0, d1, T):
             if E[c + lp] <= T:
                 done += n
                 lat += sum(E[c + lp] - x for x in coh)
+                cbi += n * (c + lp - 1)      # completes in batch c+l' (0-based index c+l'-1)
             else:
                 after += n
+    # waiting inventory the decision of batch b reads (reading R32): every
+    # arrival visible at its start S_b minus the (b-1) n admitted before
+    waiting = sum(sum(1 for x in a if x <= S[b - 1]) - (b - 1) * n for b in range(1, nb + 1))
     return dict(batches=nb, completed=done, lat=lat, ttft=ttft, first_tokens=nft,
-                completed_after_T=after, busy=sum(E[i + 1] - S[i] for i in range(nb)))
+                completed_after_T=after, busy=sum(E[i + 1] - S[i] for i in range(nb)),
+                completion_batch_idx=cbi, sum_waiting=waiting)
 
 
 def _check_maxplus(wl, n, seed_rep=0):
@@ -339,7 +346,8 @@ def _check_maxplus(wl, n, seed_rep=0):
     ref = _wait_maxplus(t.tolist(), n, l, lp, d0, d1, T)
     rows = oracle.run(wl, W.Policy(W.WAIT), [n], n_reps=1, rep_begin=seed_rep)
     assert rows[F["evictions"], 0] == 0
-    for k in ["batches", "completed", "first_tokens", "completed_after_T"]:
+    for k in ["batches", "completed", "first_tokens", "completed_after_T", "completion_batch_idx",
+              "sum_waiting"]:
         assert int(rows[F[k], 0]) == ref[k], k
     assert oracle.u128(rows, "lat")[0] == ref["lat"]
     assert oracle.u128(rows, "ttft")[0] == ref["ttft"]
@@ -519,6 +527,8 @@ def test_bruteforce_tiny_traces():
                         assert int(rows[F["batches"], i]) == ref["batches"]
                         assert int(rows[F["completed"], i]) == ref["completed"]
                         assert int(rows[F["lat_lo"], i]) == ref["lat"]
+                        assert int(rows[F["completion_batch_idx"], i]) == ref["completion_batch_idx"]
+                        assert int(rows[F["sum_waiting"], i]) == ref["sum_waiting"]
                         cnt += 1
     assert cnt > 1000
 
@@ -610,3 +620,91 @@ def test_time_varying_validation_reduces_to_constant_case():
     tv = W.c3a_time_varying()
     sup2, _, ok2 = fl.validate_time_varying(tv, seg, n, dT)
     assert sup2 == dT * sum(fl.Fr(x) * fl.Fr(1.5) for x in W.C3A.lam) and not ok2
+
+
+# ------------------------------------- hand traces (Alg. 2, FCFS budget)
+import hand_traces as H
+
+
+def _check_hand(wl, pol, thr, trace, T_s, log_exp, row_exp):
+    rows, log = oracle.run_trace(wl, pol, thr, [trace], log_cap=64, horizon_s=T_s)
+    assert [tuple(int(x) for x in r) for r in log] == log_exp
+    assert H.row_matches(rows, 0, row_exp, F, oracle.u128) == {}
+
+
+def test_nested_three_segments_hand_trace():
+    """Nested WAIT with L = 3 segments by hand (tests/hand_traces.py): the
+    k* prefix rule (b9: segment 3 passes, segment 2 fails, so
+    only segment 1 runs), ">= n_k" at equality (b4), oldest-first
+    min{n_k, Q_{k,s}} at an entry stage holding more than n_k (line 1642;
+    b10), paused later segments keeping KV in the peak (line 1643), and
+    completion at the true l' at an entry stage and mid-segment (b8)."""
+    _check_hand(H.nested_workload(H.NESTED_A_M), H.NESTED_POLICY, H.NESTED_THR, H.NESTED_TRACE,
+                H.NESTED_T_S, H.NESTED_A_LOG, H.NESTED_A_ROW)
+
+
+def test_nested_three_segments_hand_trace_eviction():
+    """Same trace with M = 100,000: paused residents' KV makes b10 overflow,
+    LIFO evicts the last admitted (P9), the restart queues
+    behind P10 (R7) and the two newest prompts evict each other in turn --
+    the eviction cascade."""
+    _check_hand(H.nested_workload(H.NESTED_B_M), H.NESTED_POLICY, H.NESTED_THR, H.NESTED_TRACE,
+                H.NESTED_T_S, H.NESTED_B_LOG, H.NESTED_B_ROW)
+
+
+def test_fcfs_token_budget_hand_trace():
+    """FCFS per-iteration prefill-token budget by hand: equality admits, the
+    first failing prompt stops admission (no skipping ahead)."""
+    _check_hand(H.fcfs_workload(), H.FCFS_POLICY, [0], H.FCFS_TRACE, 10.0, H.FCFS_LOG, H.FCFS_ROW)
+
+
+def test_p14_stage_counts_never_exceed_thresholds():
+    """P14 (Alg. 1 line 1485 / Alg. 2 'Advance min{n_k, Q_{k,s}}', by
+    induction): the oracle checks WAIT Q_{j,s} <= n_j and Nested non-entry
+    Q_{k,s} <= n_k at every decision epoch and flags a violation with status
+    3; heavy load with LIFO eviction (C4 rho = 0.95) and C3a never trip it."""
+    for wl, pol, thr in [(W.c4(4), W.Policy(W.WAIT), [18, 12, 6]),
+                         (W.c4(4), W.Policy(W.NESTED, seg_end=[100, 200, 300]), [7, 5, 2]),
+                         (W.C3A, W.Policy(W.NESTED, seg_end=[20, 40, 80, 160]), [7, 7, 7, 5])]:
+        rows = oracle.run(wl, pol, thr, n_reps=4, n_threads=4, horizon_s=5.0)
+        assert (rows[F["status"]] == 0).all()
+        assert rows[F["batches"]].min() > 20
+
+
+# ------------------------------------------------- P17 Kingman, P19 Thm 2
+def test_p17_kingman_queue_bounds():
+    """P17: the mean post-service queue at batch epochs, (sum_waiting -
+    n batches) / batches, is at most Kingman's bound 2n + lambda dT / (2(n -
+    lambda dT)) (PAPER.md:2249 WAIT; 2286 Nested segment 1) plus 3 SE, with
+    dT = d0 + d1 M^pi the full-batch time."""
+    cases = [(W.C1P, W.Policy(W.WAIT), [1], fl.wait_memory(W.C1P, [1]), 74.0, 1),
+             (W.C3A, W.Policy(W.NESTED, seg_end=[20, 40, 80, 160]), [7, 7, 7, 5],
+              fl.nested_memory_exact(W.C3A, [20, 40, 80, 160], [7, 7, 7, 5]), sum(W.C3A.lam), 7)]
+    for wl, pol, thr, mpi, lam, n in cases:
+        rows = oracle.run(wl, pol, thr, n_reps=64, n_threads=8, horizon_s=20.0)
+        assert (rows[F["evictions"]] == 0).all()
+        b = rows[F["batches"]].astype(float)
+        q = (rows[F["sum_waiting"]].astype(float) - n * b) / b
+        assert q.min() >= 0
+        a = lam * (wl.d0_s + wl.d1_s * float(mpi))
+        bound = 2 * n + a / (2 * (n - a))
+        assert q.mean() <= bound + 3 * q.std(ddof=1) / math.sqrt(len(q))
+
+
+def test_p19_thm2_memory_budget_c3a():
+    """P19: with M = infinity, the fraction of C3a replications whose peak KV
+    exceeds the Thm-2 budget (83,666 at delta = 0.1 over B ~ 1,357 batches,
+    PAPER.md:1692-1712) is at most delta (+3 binomial SE); the peaks do
+    exceed the fluid M^pi = 80,550 (queues of later segments take memory)."""
+    seg, thr = [20, 40, 80, 160], [7, 7, 7, 5]
+    big = W.Workload("c3a-inf", list(W.C3A.lam), list(W.C3A.l_tab), list(W.C3A.lp_tab),
+                     M=10 ** 9, horizon_s=W.C3A.horizon_s, seed=W.C3A.seed)
+    n = 160
+    rows = oracle.run(big, W.Policy(W.NESTED, seg_end=seg), thr, n_reps=n, n_threads=8)
+    B = float(rows[F["batches"]].mean())
+    assert abs(B - 1357) < 0.05 * 1357
+    _, _, _, budget = fl.thm2_budget(W.C3A, seg, thr, round(B), 0.1)
+    peak = rows[F["max_kv_peak"]].astype(float)
+    frac = float(np.mean(peak > budget))
+    assert frac <= 0.1 + 3 * math.sqrt(0.1 * 0.9 / n)
+    assert peak.max() > 80550
