@@ -104,7 +104,11 @@ typedef struct {
   uint32_t max_resident;      /* per-replication safe resident capacity (0 = derive): the
                                  fallback launch's; the main launch still runs with a
                                  speculative capacity <= it (see spec_resident) */
-  uint32_t restart_cap;       /* per-FIFO restart ring capacity (0 = default 8192) */
+  uint32_t restart_cap;       /* restart pool capacity in entries (0 = default 2^24): evicted
+                                 prompts waiting to re-enter their FIFO live in
+                                 64-entry chunks of one device pool shared by all replications
+                                 of a launch (20 B per entry); a replication finding it
+                                 exhausted reports status 2 */
   /* optional time-varying rates ("Time-Varying Arrival
    * Rates"; NULL rf_off = all homogeneous): class c has pieces
    * [rf_off[c], rf_off[c+1]) of (rf_t start second, rf_rate rate >= 0) with
@@ -195,7 +199,7 @@ int sched_run_trace(sched_t h, const int64_t* t_ticks, const int32_t* cls,
 /* Launch configuration used by sched_run (for roofline accounting). */
 typedef struct {
   int32_t grid, block, warps_per_block, shared_bytes, blocks_per_sm, sm_count;
-  int32_t max_resident, restart_cap;      /* safe capacity, ring capacity */
+  int32_t max_resident, restart_cap;      /* safe capacity, restart pool entries */
   int32_t spec_resident;                  /* main-launch capacity (== max_resident: no fallback) */
   int32_t fallback_grid, fallback_warps_per_block;
   int32_t engine;                         /* 0 member engine (per-resident records, every
@@ -208,6 +212,12 @@ typedef struct {
                                              is first launched, forces one. */
 } sched_launch_info;
 int sched_get_launch_info(sched_t h, sched_launch_info* out);
+
+/* Restart pool use (synchronous device read): capacity in entries and the
+ * high-water mark (entries in chunks ever handed out; freed chunks are
+ * reused first, so this bounds the concurrent peak).  Errors: SCHED_E_INVALID,
+ * SCHED_E_CUDA. */
+int sched_restart_pool_stats(sched_t h, uint64_t* capacity_entries, uint64_t* high_water_entries);
 
 /* NEXT(4): the appendix's embedded random-walk chains, one thread per walk
  * (App. B-C).  kind 0: the WAIT chain of Lemma

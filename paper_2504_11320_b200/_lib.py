@@ -31,8 +31,8 @@ F = {n: i for i, n in enumerate(FIELDS)}
 
 # every symbol include/sched.h declares
 EXPORTS = ["sched_create", "sched_thresholds", "sched_run", "sched_run_host",
-           "sched_run_trace", "sched_get_launch_info", "sched_walks", "sched_walks_host",
-           "sched_destroy", "sched_last_error"]
+           "sched_run_trace", "sched_get_launch_info", "sched_restart_pool_stats", "sched_walks",
+           "sched_walks_host", "sched_destroy", "sched_last_error"]
 WALK_FIELDS = ["W_B", "stuck", "sumW", "maxW", "Wt_B", "viol", "sumX", "maxS", "minS", "S_B"]
 WF = {n: i for i, n in enumerate(WALK_FIELDS)}
 
@@ -104,6 +104,7 @@ def lib() -> C.CDLL:
                                       C.c_void_p, C.c_uint32, C.c_double, C.c_void_p, C.c_void_p,
                                       C.c_int64, C.POINTER(C.c_int64)]
         L.sched_get_launch_info.argtypes = [C.c_void_p, C.POINTER(LaunchInfo)]
+        L.sched_restart_pool_stats.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.sched_destroy.argtypes = [C.c_void_p]
         L.sched_walks.argtypes = [C.c_int32, C.c_int64, C.c_double, C.c_int64, C.c_double,
                                   C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p,
@@ -112,8 +113,8 @@ def lib() -> C.CDLL:
                                        C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p,
                                        C.c_int32]
         for name in ["sched_create", "sched_thresholds", "sched_run", "sched_run_host",
-                     "sched_run_trace", "sched_get_launch_info", "sched_walks",
-                     "sched_walks_host"]:
+                     "sched_run_trace", "sched_get_launch_info", "sched_restart_pool_stats",
+                     "sched_walks", "sched_walks_host"]:
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -227,6 +228,13 @@ class Scheduler:
         _check(lib().sched_get_launch_info(self._h, C.byref(li)))
         return {n: getattr(li, n) for n, _ in LaunchInfo._fields_}
 
+    def restart_pool(self) -> dict:
+        """Restart pool capacity and high-water mark, in entries (20 B each)."""
+        cap, hw = C.c_uint64(0), C.c_uint64(0)
+        _check(lib().sched_restart_pool_stats(self._h, C.byref(cap), C.byref(hw)))
+        return {"capacity_entries": cap.value, "high_water_entries": hw.value,
+                "high_water_bytes": hw.value * 20}
+
     def run_device(self, seed: int, rep_begin: int, n_reps: int, horizon_s: float,
                    out_ptr: int, stream_ptr: int = 0):
         """Asynchronous launch; out_ptr = device pointer to NF * n_reps uint64."""
@@ -238,6 +246,9 @@ class Scheduler:
         """Rows [NF, n_reps] (uint64) through a host buffer (H2D/D2H inside)."""
         if out is None:
             out = np.zeros((NF, n_reps), dtype=np.uint64)
+        # sched_run_host writes NF * n_reps uint64 through this pointer
+        if out.dtype != np.uint64 or out.shape != (NF, n_reps) or not out.flags.c_contiguous:
+            raise ValueError(f"out must be a C-contiguous uint64 array of shape {(NF, n_reps)}")
         _check(lib().sched_run_host(self._h, seed, rep_begin, n_reps, horizon_s,
                                     out.ctypes.data, C.c_void_p(stream_ptr)))
         return out

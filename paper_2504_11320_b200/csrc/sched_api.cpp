@@ -50,7 +50,8 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 struct sched_s {
   SetupInput in;
-  uint32_t tok_budget = 0, max_resident_cfg = 0, spec_resident_cfg = 0, ring_cap = 8192;
+  uint32_t tok_budget = 0, max_resident_cfg = 0, spec_resident_cfg = 0;
+  uint64_t pool_entries = 1ull << 24;  // restart pool capacity (entries), shared by a launch
   int device = 0;
   int64_t d0_t = 0, d1_t = 0;
   uint32_t max_lp = 0, min_l = 0;
@@ -70,10 +71,13 @@ struct sched_s {
   double* d_rf_scale = nullptr;
   bool tv_any = false;
   // scratch
-  int64_t* d_ring_a = nullptr;
-  int64_t* d_ring_e = nullptr;
-  uint32_t* d_ring_llp = nullptr;
-  size_t ring_entries = 0;
+  // restart-FIFO chunk pool
+  int64_t* d_pool_a = nullptr;
+  int64_t* d_pool_e = nullptr;
+  uint32_t* d_pool_llp = nullptr;
+  uint32_t* d_pool_next = nullptr;
+  unsigned long long* d_pool_free = nullptr;  // [0] free-stack head, [1] bump counter (low word)
+  uint32_t pool_chunks = 0;
   uint32_t* d_counter = nullptr;
   uint64_t* d_out = nullptr;
   size_t out_cap = 0;
@@ -239,7 +243,8 @@ int prepare(sched_s* h) {
   }
   // choose warps per block maximising resident warps per SM
   auto size_launch = [&](bool ring, uint32_t records, uint32_t* wsm, int* wpb_out, int* bps_out) -> int {
-    *wsm = warp_smem_bytes(records, K, h->tv_any, ring, h->in.policy == SCHED_NESTED);
+    *wsm = warp_smem_bytes(records, K, h->tv_any, ring, h->in.policy == SCHED_NESTED,
+                           h->in.policy == SCHED_WAIT ? (uint32_t)K : 1u);
     int best_w = 0;
     const int cands[] = {8, 4, 2, 1};
     for (int wpb : cands) {
@@ -349,7 +354,13 @@ int prepare(sched_s* h) {
       const bool binds = in.policy == SCHED_WAIT ? mpi > (double)in.M : h->m_star > (double)in.M;
       L.spare = binds ? 32u : 8u;
     }
-    if (int rc = size_cfg(L)) return rc;
+    // a ring footprint that does not fit in shared memory only makes the
+    // ring engine ineligible (the member engine runs), unless it was forced
+    const bool forced = eng && std::string(eng) == "ring";
+    if (int rc = size_cfg(L)) {
+      if (forced) return rc;
+      L.grid = 0;
+    }
     // the ring engine does O(classes + events) work per batch but its
     // per-class capacities can cost occupancy: keep it unless its
     // speculative footprint exceeds the member engine's by > 30%
@@ -364,33 +375,38 @@ int prepare(sched_s* h) {
     double lam = 0, lam_lp = 0;
     for (int c = 0; c < K; ++c) { lam += in.lambda[c]; lam_lp += in.lambda[c] * in.lp[c][0].first; }
     const bool short_lp = lam > 0 && lam_lp / lam <= 64.0;
-    const bool forced = eng && std::string(eng) == "ring";
-    h->use_ring = forced || h->spec_resident_cfg ||
-                  ((double)ring_rec <= 1.3 * (double)h->mem.Rc && (in.policy == SCHED_WAIT || short_lp));
+    h->use_ring = L.grid > 0 && (forced || ((double)ring_rec <= 1.3 * (double)h->mem.Rc &&
+                                            (in.policy == SCHED_WAIT || short_lp)));
   }
   const int n_rings = h->in.policy == SCHED_WAIT ? K : 1;
-  size_t slots = (size_t)std::max(h->mem.grid * h->mem.wpb, h->mem.fb_grid * h->mem.fb_wpb);
-  if (h->use_ring)
-    slots = std::max(slots, (size_t)std::max(h->rng.grid * h->rng.wpb, h->rng.fb_grid * h->rng.fb_wpb));
-  const size_t need = slots * n_rings * h->ring_cap;
-  if (need > h->ring_entries) {
-    cudaFree(h->d_ring_a); cudaFree(h->d_ring_e); cudaFree(h->d_ring_llp);
-    h->d_ring_a = h->d_ring_e = nullptr; h->d_ring_llp = nullptr;
-    CK(cudaMalloc(&h->d_ring_a, need * 8));
-    CK(cudaMalloc(&h->d_ring_e, need * 8));
-    CK(cudaMalloc(&h->d_ring_llp, need * 4));
-    h->ring_entries = need;
+  if (!h->d_pool_a) {
+    // one pool of restart-FIFO chunks for every replication of a launch:
+    // memory follows the evictions that actually wait, not warps x capacity
+    const uint64_t chunks = std::max<uint64_t>(1, h->pool_entries / kRestartChunk);
+    if (chunks >= kNoChunk) return fail(SCHED_E_INVALID, "restart pool too large");
+    h->pool_chunks = (uint32_t)chunks;
+    const size_t n = (size_t)chunks * kRestartChunk;
+    CK(cudaMalloc(&h->d_pool_a, n * 8));
+    CK(cudaMalloc(&h->d_pool_e, n * 8));
+    CK(cudaMalloc(&h->d_pool_llp, n * 4));
+    CK(cudaMalloc(&h->d_pool_next, (size_t)chunks * 4));
+    CK(cudaMalloc(&h->d_pool_free, 16));
+    const unsigned long long init[2] = {(unsigned long long)kNoChunk, 0ull};  // empty stack, nothing handed out
+    CK(cudaMemcpy(h->d_pool_free, init, 16, cudaMemcpyHostToDevice));
   }
   if (!h->d_counter) CK(cudaMalloc(&h->d_counter, 16));  // [main, fallback, retry count]
   DevParams& p = h->base;
   p.n_rings = n_rings;
-  p.ring_cap = h->ring_cap;
   for (size_t i = 0; i < h->in.thresholds.size() && i < 32; ++i) p.thr[i] = h->in.thresholds[i];
   for (int c = 0; c < K; ++c)
     p.fl[c] = (uint32_t)h->in.l[c][0].first | ((uint32_t)h->in.lp[c].back().first << 16);
-  p.ring_a = h->d_ring_a;
-  p.ring_e = h->d_ring_e;
-  p.ring_llp = h->d_ring_llp;
+  p.pool_a = h->d_pool_a;
+  p.pool_e = h->d_pool_e;
+  p.pool_llp = h->d_pool_llp;
+  p.pool_next = h->d_pool_next;
+  p.pool_free = h->d_pool_free;
+  p.pool_bump = (uint32_t*)(h->d_pool_free + 1);
+  p.pool_chunks = h->pool_chunks;
   p.work_counter = h->d_counter;
   h->prepared = true;
   return 0;
@@ -595,7 +611,7 @@ int sched_create(sched_t* out, const sched_config* cfg) {
   h->tok_budget = cfg->tok_budget;
   h->max_resident_cfg = cfg->max_resident;
   h->spec_resident_cfg = cfg->spec_resident;
-  if (cfg->restart_cap) h->ring_cap = cfg->restart_cap;
+  if (cfg->restart_cap) h->pool_entries = cfg->restart_cap;
   h->device = cfg->device;
   // ticks
   h->d0_t = std::llround(cfg->d0_s * 1e12);
@@ -783,11 +799,23 @@ int sched_get_launch_info(sched_t h, sched_launch_info* out) {
   out->blocks_per_sm = L.blocks_per_sm;
   out->sm_count = h->sm_count;
   out->max_resident = (int32_t)safe;
-  out->restart_cap = (int32_t)h->ring_cap;
+  out->restart_cap = (int32_t)std::min<uint64_t>(h->pool_entries, INT32_MAX);
   out->spec_resident = (int32_t)spec;
   out->fallback_grid = L.fallback ? L.fb_grid : 0;
   out->fallback_warps_per_block = L.fallback ? L.fb_wpb : 0;
   out->engine = L.ring ? 1 : 0;
+  return SCHED_OK;
+}
+
+int sched_restart_pool_stats(sched_t h, uint64_t* capacity_entries, uint64_t* high_water_entries) {
+  if (!h || !capacity_entries || !high_water_entries) return fail(SCHED_E_INVALID, "null argument");
+  *capacity_entries = (uint64_t)h->pool_chunks * kRestartChunk;
+  *high_water_entries = 0;
+  if (!h->d_pool_free) return SCHED_OK;  // never launched
+  CK(cudaSetDevice(h->device));
+  uint32_t bump = 0;
+  CK(cudaMemcpy(&bump, h->d_pool_free + 1, 4, cudaMemcpyDeviceToHost));
+  *high_water_entries = (uint64_t)std::min(bump, h->pool_chunks) * kRestartChunk;
   return SCHED_OK;
 }
 
@@ -845,9 +873,11 @@ void sched_destroy(sched_t h) {
   cudaFree(h->d_cdf_val);
   cudaFree(h->d_cdf_guide);
   cudaFree(h->d_stage_info);
-  cudaFree(h->d_ring_a);
-  cudaFree(h->d_ring_e);
-  cudaFree(h->d_ring_llp);
+  cudaFree(h->d_pool_a);
+  cudaFree(h->d_pool_e);
+  cudaFree(h->d_pool_llp);
+  cudaFree(h->d_pool_next);
+  cudaFree(h->d_pool_free);
   cudaFree(h->d_counter);
   cudaFree(h->d_out);
   cudaFree(h->d_retry);

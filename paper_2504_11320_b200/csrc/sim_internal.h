@@ -8,6 +8,8 @@ namespace waitsim {
 constexpr int kMaxClasses = 32;
 constexpr int kMaxSegments = 32;
 constexpr int kLanes = 32;
+constexpr uint32_t kRestartChunk = 64;    // restart-FIFO entries per pool chunk
+constexpr uint32_t kNoChunk = 0xFFFFFFFFu;
 
 struct ClassParam {
   double gap_scale;        // 1e12 / lambda (ticks per unit exponential); 0 = no arrivals
@@ -37,7 +39,6 @@ struct DevParams {
   uint32_t rcap[kMaxClasses];      // ring capacity (records) of class c
   uint32_t roff[kMaxClasses];      // first record of ring c after the staging area
   uint32_t fl[kMaxClasses];        // fixed l | l' << 16 of class c
-  uint32_t ring_cap;       // restart ring capacity (entries) per ring
   uint32_t warp_smem;      // bytes of shared memory per warp
   uint64_t seed;
   uint64_t rep_begin;      // global index of local replication 0
@@ -60,10 +61,17 @@ struct DevParams {
   const uint16_t* tr_l;
   const uint16_t* tr_lp;
   const int64_t* tr_off;   // [n_reps*K + 1]
-  // scratch
-  int64_t* ring_a;
-  int64_t* ring_e;
-  uint32_t* ring_llp;
+  // restart FIFOs (evicted prompts): linked lists of
+  // kRestartChunk-entry chunks from one device-wide pool shared by every
+  // replication of the launch; free chunks on a lock-free
+  // stack (head = tag << 32 | chunk), never-used ones from a bump counter
+  int64_t* pool_a;         // [chunks * kRestartChunk] original arrival tick
+  int64_t* pool_e;         // eviction tick
+  uint32_t* pool_llp;      // l | l' << 16 | first-token << 31 (ring engine: class | ft << 31)
+  uint32_t* pool_next;     // [chunks] next chunk of a FIFO / of the free stack
+  unsigned long long* pool_free;  // free-stack head
+  uint32_t* pool_bump;     // chunks handed out so far (high-water mark)
+  uint32_t pool_chunks;
   uint32_t* work_counter;  // this launch's replication counter
   // speculative capacity: the main launch runs with a small resident
   // capacity; replications that overflow it are appended to retry_list and
@@ -79,7 +87,8 @@ struct DevParams {
 };
 
 // shared-memory bytes per warp for a given resident capacity / class count
-inline uint32_t warp_smem_bytes(uint32_t Rc, int K, bool tv = false, bool ring = false, bool nested = false) {
+inline uint32_t warp_smem_bytes(uint32_t Rc, int K, bool tv = false, bool ring = false, bool nested = false,
+                                uint32_t n_rings = 1) {
   uint32_t b = Rc * 16u;                    // residents: a (i64) + packed (l, l', s, meta)
   b += (uint32_t)K * (32u * 12u);           // generated windows (t, l, l')
   b += (uint32_t)K * (32u * 12u);           // private admission windows (t, l, l')
@@ -89,7 +98,9 @@ inline uint32_t warp_smem_bytes(uint32_t Rc, int K, bool tv = false, bool ring =
   if (ring) b += 256u;                      // class-ring eviction scratch
   if (nested) b += ((Rc + 31u) / 32u + 15u) & ~15u;  // per-chunk activity summaries
   if (tv) b += (uint32_t)K * (32u * 16u);   // operational-time windows (generated, private)
-  return (b + 15u) & ~15u;
+  b = (b + 15u) & ~15u;
+  b += (n_rings * 12u + 15u) & ~15u;        // restart FIFO chunk cursors (head, head index, tail)
+  return b;
 }
 
 cudaError_t launch_sim(const DevParams& p, int grid, int block, size_t smem, cudaStream_t s);

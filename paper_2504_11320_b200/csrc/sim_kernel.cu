@@ -289,7 +289,7 @@ struct WarpSim {
   WarpStats* st;                     // metric accumulators
   uint64_t* xs;                      // [32] RING eviction scratch (per-class sums)
   uint8_t* csum;                     // NESTED: per-chunk lowest resident segment
-  size_t ring_base;                  // first ring entry of this warp slot
+  uint32_t* rq;                      // [n_rings][4] restart FIFO chunks: head, head index, tail, tail index
 
   // per-class cursor state, lane c holds class c (and ring c for WAIT; ring 0
   // otherwise).  The generated window [vbase, vbase+32) serves visibility
@@ -325,8 +325,8 @@ struct WarpSim {
   uint32_t n_plan_res;
   bool below;         // no batch because of the threshold test (idle skip allowed)
 
-  __device__ WarpSim(const DevParams& p, unsigned char* base, int lane_, size_t rb)
-      : P(p), lane(lane_), ring_base(rb) {
+  __device__ WarpSim(const DevParams& p, unsigned char* base, int lane_)
+      : P(p), lane(lane_) {
     const uint32_t Rc = p.Rc;
     rr = (Rec*)base;
     // RING: 32 spare staging slots hold the victims of one eviction round
@@ -349,6 +349,7 @@ struct WarpSim {
     vtau = (int64_t*)((unsigned char*)st + (RING ? 512 : 256) +
                       (POL == SCHED_NESTED ? (((p.Rc + 31) / 32 + 15) & ~15u) : 0u));
     atau = vtau + p.K * 32;
+    rq = (uint32_t*)(base + p.warp_smem - ((p.n_rings * 12u + 15u) & ~15u));
   }
 
   __device__ void flush_acc() {
@@ -360,8 +361,93 @@ struct WarpSim {
     if (__any_sync(FULL, ((acc_arr | acc_done_a | acc_ft_a) >> 60) != 0)) flush_acc();
   }
 
-  __device__ __forceinline__ size_t ring_slot(int q, uint32_t pos) const {
-    return ring_base + (size_t)q * P.ring_cap + (pos % P.ring_cap);
+  // ------------------------------------------- restart FIFOs (chunk pool)
+  // FIFO q holds positions [rhead, rtail) (lane q's counters) in a linked
+  // list of kRestartChunk-entry chunks: rq[4q] = chunk of position
+  // rhead (index rq[4q+1] = its position / kRestartChunk), rq[4q+2] = chunk
+  // of the next write position rtail (index rq[4q+3]).  Chunks come from the
+  // device-wide pool: a lock-free free stack (ABA tag in the high word), else
+  // never-used chunks; a chunk is returned when the committed head passes it
+  // and at the end of the replication.
+  __device__ uint32_t pool_alloc() const {
+    unsigned long long old = atomicAdd(P.pool_free, 0ull);
+    while ((uint32_t)old != kNoChunk) {
+      const uint32_t nxt = __ldcg(P.pool_next + (uint32_t)old);
+      const unsigned long long nw = (((old >> 32) + 1ull) << 32) | nxt;
+      const unsigned long long prev = atomicCAS(P.pool_free, old, nw);
+      if (prev == old) return (uint32_t)old;
+      old = prev;
+    }
+    const uint32_t c = atomicAdd(P.pool_bump, 1u);
+    return c < P.pool_chunks ? c : kNoChunk;
+  }
+  __device__ void pool_release(uint32_t c) const {
+    unsigned long long old = atomicAdd(P.pool_free, 0ull);
+    for (;;) {
+      __stcg(P.pool_next + c, (uint32_t)old);
+      __threadfence();
+      const unsigned long long nw = (((old >> 32) + 1ull) << 32) | c;
+      const unsigned long long prev = atomicCAS(P.pool_free, old, nw);
+      if (prev == old) return;
+      old = prev;
+    }
+  }
+  // pool entry of position pos (>= the committed head) of FIFO q
+  __device__ __forceinline__ size_t fifo_entry(int q, uint32_t pos) const {
+    uint32_t c = rq[4 * q], ci = rq[4 * q + 1];
+    for (const uint32_t want = pos / kRestartChunk; ci < want; ++ci) c = __ldcg(P.pool_next + c);
+    return (size_t)c * kRestartChunk + pos % kRestartChunk;
+  }
+  // pool entry of tail position pos (the tail chunk or the one after it)
+  __device__ __forceinline__ size_t fifo_wentry(int q, uint32_t pos) const {
+    uint32_t c = rq[4 * q + 2];
+    if (pos / kRestartChunk != rq[4 * q + 3]) c = __ldcg(P.pool_next + c);
+    return (size_t)c * kRestartChunk + pos % kRestartChunk;
+  }
+  // lane q: chunks for cnt (<= 32) more entries at the tail t of FIFO q
+  // (the chunk of the next write position included); false: pool exhausted
+  __device__ bool fifo_reserve(int q, uint32_t t, uint32_t cnt) const {
+    if (rq[4 * q + 2] == kNoChunk) {
+      const uint32_t c = pool_alloc();
+      if (c == kNoChunk) return false;
+      rq[4 * q] = rq[4 * q + 2] = c;
+      rq[4 * q + 1] = rq[4 * q + 3] = t / kRestartChunk;
+    }
+    if ((t + cnt) / kRestartChunk > rq[4 * q + 3]) {
+      const uint32_t c = pool_alloc();
+      if (c == kNoChunk) return false;
+      __stcg(P.pool_next + rq[4 * q + 2], c);
+    }
+    return true;
+  }
+  // lane q, after the writes: the tail chunk follows the new tail position
+  __device__ void fifo_tail_done(int q, uint32_t t_new) const {
+    if (t_new / kRestartChunk > rq[4 * q + 3]) {
+      rq[4 * q + 2] = __ldcg(P.pool_next + rq[4 * q + 2]);
+      rq[4 * q + 3] += 1;
+    }
+  }
+  // lane q: return the chunks the committed head has passed
+  __device__ void fifo_commit(int q, uint32_t head) const {
+    while (rq[4 * q + 2] != kNoChunk && rq[4 * q + 1] < head / kRestartChunk) {
+      const uint32_t c = rq[4 * q];
+      rq[4 * q] = __ldcg(P.pool_next + c);
+      rq[4 * q + 1] += 1;
+      pool_release(c);
+    }
+  }
+  // lane q: return every chunk of FIFO q (end of the replication)
+  __device__ void fifo_release_all(int q) const {
+    if (rq[4 * q + 2] == kNoChunk) return;
+    uint32_t c = rq[4 * q];
+    for (;;) {
+      const uint32_t nxt = __ldcg(P.pool_next + c);
+      const bool last = c == rq[4 * q + 2];
+      pool_release(c);
+      if (last) break;
+      c = nxt;
+    }
+    rq[4 * q] = rq[4 * q + 2] = kNoChunk;
   }
   // NESTED stage info: segment index (bits 0-5), last stage of the segment
   // (bit 6), entry stage (bit 7); counter slot = segment (+32 at entry)
@@ -804,7 +890,7 @@ struct WarpSim {
       const uint32_t h0 = bcast32(rhead, q);
       if (nr > 0) {
         __syncwarp();
-        if ((uint32_t)lane < nr) re[lane] = P.ring_e[ring_slot(q, h0 + lane)];
+        if ((uint32_t)lane < nr) re[lane] = __ldcg(P.pool_e + fifo_entry(q, h0 + lane));
         __syncwarp();
       }
       const uint32_t ncand = total + nr;
@@ -848,9 +934,9 @@ struct WarpSim {
             r += count_before(re, nr, key, false);       // restarts with e < t
           } else {
             key = re[pos];
-            const size_t e = ring_slot(q, h0 + pos);
-            a = P.ring_a[e];
-            const uint32_t llp = P.ring_llp[e];
+            const size_t e = fifo_entry(q, h0 + pos);
+            a = __ldcg(P.pool_a + e);
+            const uint32_t llp = __ldcg(P.pool_llp + e);
             uint32_t cls = POL == SCHED_WAIT ? (uint32_t)q : 0u;
             if (RING) {  // {class, ft}: the class fixes l, l'
               cls = llp & 0xFFu;
@@ -1033,25 +1119,26 @@ struct WarpSim {
       const uint32_t grp = __match_any_sync(FULL, key);
       const uint32_t before = __popc(grp & lanemask_lt());
       const uint32_t tail_q = __shfl_sync(FULL, rtail, q);
-      const uint32_t head_q = __shfl_sync(FULL, rhead, q);
-      const bool overflow = ev && (tail_q - head_q + before + 1 > P.ring_cap);
-      if (__any_sync(FULL, overflow)) { status = 2; return; }
+      // victims per restart FIFO (lane q owns FIFO q): reserve pool chunks
+      uint32_t my_cnt = POL == SCHED_WAIT ? 0u : (lane == 0 ? ne : 0u);
+      if (POL == SCHED_WAIT)
+        for (int c = 0; c < P.K; ++c) {
+          const uint32_t mm = __ballot_sync(FULL, ev && q == c);
+          if (lane == c) my_cnt = __popc(mm);
+        }
+      const bool res_ok = my_cnt == 0 || fifo_reserve(lane, rtail, my_cnt);
+      if (__any_sync(FULL, !res_ok)) { status = 2; return; }
+      __syncwarp();
       if (ev) {
-        const size_t e = ring_slot(q, tail_q + before);
-        P.ring_a[e] = a;
-        P.ring_e[e] = now;
-        P.ring_llp[e] = l | (lp << 16) | ((meta & META_FT) ? 0x80000000u : 0u);
+        const size_t e = fifo_wentry(q, tail_q + before);
+        P.pool_a[e] = a;
+        P.pool_e[e] = now;
+        P.pool_llp[e] = l | (lp << 16) | ((meta & META_FT) ? 0x80000000u : 0u);
         if (POL == SCHED_WAIT) sh_add_u32(&cnt[meta & 0xFF], ~0u);
         if (POL == SCHED_NESTED) sh_add_u32(&cnt[nkey], ~0u);
       }
-      if (POL == SCHED_WAIT) {  // advance ring tails (lane q owns ring q)
-        for (int c = 0; c < P.K; ++c) {
-          const uint32_t mm = __ballot_sync(FULL, ev && q == c);
-          if (lane == c) rtail += __popc(mm);
-        }
-      } else if (lane == 0) {
-        rtail += ne;
-      }
+      __syncwarp();
+      if (my_cnt) { rtail += my_cnt; fifo_tail_done(lane, rtail); }
       excess -= (int64_t)__reduce_add_sync(FULL, ev ? f : 0u);
       KV -= (int64_t)__reduce_add_sync(FULL, ev ? (l + s - 1) : 0u);
       n_plan_res -= __reduce_add_sync(FULL, ev ? inp : 0u);
@@ -1160,17 +1247,24 @@ struct WarpSim {
       const int q = POL == SCHED_WAIT ? (int)v : 0;
       const uint32_t grp = __match_any_sync(FULL, ev ? (uint32_t)q : (0x100u + (uint32_t)lane));
       const uint32_t before = __popc(grp & lanemask_lt());
-      const uint32_t tail_q = __shfl_sync(FULL, rtail, q), head_q = __shfl_sync(FULL, rhead, q);
-      if (__any_sync(FULL, ev && (tail_q - head_q + before + 1 > P.ring_cap))) { status = 2; return; }
+      const uint32_t tail_q = __shfl_sync(FULL, rtail, q);
+      uint32_t my_cnt = POL == SCHED_WAIT ? 0u : (lane == 0 ? ne : 0u);
+      if (POL == SCHED_WAIT)
+        for (int c = 0; c < K; ++c) {
+          const uint32_t mm = __ballot_sync(FULL, ev && q == c);
+          if (lane == c) my_cnt = __popc(mm);
+        }
+      const bool res_ok = my_cnt == 0 || fifo_reserve(lane, rtail, my_cnt);
+      if (__any_sync(FULL, !res_ok)) { status = 2; return; }
       cnt[lane] = 0;
       xs[lane] = 0;
       __syncwarp();
       if (ev) {
-        const size_t ri = ring_slot(q, tail_q + before);
-        P.ring_a[ri] = e.a;
-        P.ring_e[ri] = now;
+        const size_t ri = fifo_wentry(q, tail_q + before);
+        P.pool_a[ri] = e.a;
+        P.pool_e[ri] = now;
         // ring engine: lengths are the class's, so the record keeps the class
-        P.ring_llp[ri] = v | (((xf & XF_FT) && !pend) ? 0x80000000u : 0u);
+        P.pool_llp[ri] = v | (((xf & XF_FT) && !pend) ? 0x80000000u : 0u);
         sh_add_u32(&cnt[v], 1u);
         sh_add_u64(&xs[v], (uint64_t)x);
         if (pend) { sh_add_u32(&cnt[32 + v], ~0u); sh_add_u64(&psum()[v], (uint64_t)(-e.a)); }
@@ -1180,9 +1274,8 @@ struct WarpSim {
         const uint32_t k = cnt[lane];
         r_n -= k;
         r_X -= xs[lane];
-        if (POL == SCHED_WAIT) rtail += k;  // ring q = class q
       }
-      if (POL != SCHED_WAIT && lane == 0) rtail += ne;
+      if (my_cnt) { rtail += my_cnt; fifo_tail_done(lane, rtail); }
       if (lane == 0) st->evictions += ne;
       excess -= (int64_t)__reduce_add_sync(FULL, ev ? f : 0u);
       KV -= (int64_t)__reduce_add_sync(FULL, ev ? (l + s - 1) : 0u);
@@ -1583,6 +1676,7 @@ struct WarpSim {
     }
     __syncwarp();
     k_vis = vbase = k_adm = abase = pcount = rhead = rtail = 0;
+    if (lane < P.n_rings) rq[4 * lane] = rq[4 * lane + 2] = kNoChunk;
     vprev = aprev = 0;
     newc = 0;
     r_head = r_n = r_C = seq_next = 0;
@@ -1616,6 +1710,8 @@ struct WarpSim {
         now = nt;
         continue;
       }
+      // admissions are final: return the restart chunks the heads passed
+      if (lane < P.n_rings) fifo_commit(lane, rhead);
       execute(n_evict, peak, waiting);
       if (RING && status) break;
     }
@@ -1624,6 +1720,7 @@ struct WarpSim {
 
   __device__ void finish() {
     const uint32_t waiting = waiting_total();
+    if (lane < P.n_rings) fifo_release_all(lane);
     flush_acc();
     __syncwarp();
     const WarpStats S = *st;
@@ -1675,9 +1772,7 @@ __global__ void __launch_bounds__(POL == SCHED_WAIT ? 128 : 256, POL == SCHED_WA
   extern __shared__ __align__(16) unsigned char smem[];
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int slot = blockIdx.x * (blockDim.x >> 5) + wib;
-  const size_t ring_base = (size_t)slot * P.n_rings * P.ring_cap;
-  WarpSim<POL, TRACE, RING> sim(P, smem + (size_t)wib * P.warp_smem, lane, ring_base);
+  WarpSim<POL, TRACE, RING> sim(P, smem + (size_t)wib * P.warp_smem, lane);
   for (;;) {
     uint32_t i = 0;
     if (lane == 0) i = atomicAdd(P.work_counter, 1u);

@@ -9,6 +9,7 @@ aggregate vector (integer counters + float64 second sums) over NCCL.
 from __future__ import annotations
 
 import os
+import sys
 from typing import Dict, Tuple
 
 import torch
@@ -34,10 +35,16 @@ def init(backend: str = None) -> Tuple[int, int, int]:
             backend = "nccl" if torch.cuda.is_available() else "gloo"
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if backend == "nccl":
+            # NCCL logs its communicator init (rank / nranks / transport) on
+            # stderr, so a launcher can see how many ranks took part
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             torch.cuda.set_device(local)
             dist.init_process_group(backend, device_id=torch.device(f"cuda:{local}"))
         else:
             dist.init_process_group(backend)
+        print(f"[dist] rank {dist.get_rank()}/{dist.get_world_size()} backend={dist.get_backend()} "
+              f"device=cuda:{local}", file=sys.stderr, flush=True)
     return rank, world, local
 
 
@@ -72,7 +79,7 @@ def allreduce_aggregates(agg: Dict[str, torch.Tensor]) -> Dict[str, torch.Tensor
     """THE collective: one all-reduce(SUM) of the packed aggregate vector.
     Integer counters travel as float64, exact while every sum stays below
     2^53 (request steps of a C2 step on 8 GPUs are ~2.6e10)."""
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+    if not (dist.is_available() and dist.is_initialized()):
         return agg
     ints, f64 = agg["int"], agg["f64"]
     buf = _all_reduce(torch.cat([ints.to(torch.float64), f64]))

@@ -44,7 +44,9 @@ AGG_F64 = ["lat", "ttft", "soj", "busy", "lat_sq", "thr_sq"]
 def aggregate(rows: torch.Tensor, horizon_s: float) -> Dict[str, torch.Tensor]:
     """Device-side sums over replications of one rows tensor (small vectors)."""
     r = rows
-    ints = torch.stack([r[F[k]].sum() for k in AGG_INT])
+    # status: the NUMBER of replications with a nonzero status (1 resident
+    # overflow, 2 restart overflow), not the sum of the codes
+    ints = torch.stack([(r[F[k]] != 0).sum() if k == "status" else r[F[k]].sum() for k in AGG_INT])
     two64 = 18446744073709551616.0
 
     def t128(name):

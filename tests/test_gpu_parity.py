@@ -100,7 +100,7 @@ def test_c4_rate_sweep(i):
 @pytest.mark.parametrize("qps", [55.0, 110.0])
 def test_c5_chat_shaped(qps):
     wl = W.c5(qps)
-    kw = dict(max_resident=4096, restart_cap=1 << 16)
+    kw = dict(max_resident=4096, restart_cap=1 << 20)
     check(wl, W.Policy(W.NESTED, seg_end=SEG10), W.PAPER_NESTED_RATIO_C5, 8, horizon_s=120.0, **kw)
     check(wl, W.Policy(W.FCFS, B=1024), [0], 8, horizon_s=120.0, **kw)
     check(wl, W.Policy(W.FCFS_ONGOING, B=1024), [0], 8, horizon_s=120.0, **kw)
@@ -476,3 +476,37 @@ def test_hand_traces_replayed(case):
     ref_rows, ref_log = oracle.run_trace(wl, pol, thr, [tr], log_cap=64, horizon_s=T)
     assert np.array_equal(log, ref_log)
     assert_rows_equal(rows, ref_rows, case)
+
+
+# ------------------------------------------------ restart pool
+def test_restart_pool_chunks_are_reused():
+    """C1 WAIT evicts ~280 prompts per replication; 16,384 replications push
+    ~4.6M restart entries through a pool of 2^18 (4,096 chunks): chunks are
+    returned and reused, every row has status 0, sampled rows equal the
+    oracle and the high-water mark stays within the pool."""
+    from paper_2504_11320_b200 import Scheduler
+    s = Scheduler(W.C1, W.Policy(W.WAIT), [1], restart_cap=1 << 18)
+    rows = s.run_host(W.C1.seed, 0, 16384, W.C1.horizon_s)
+    pool = s.restart_pool()
+    s.close()
+    assert (rows[oracle.F["status"]] == 0).all()
+    assert int(rows[oracle.F["evictions"]].astype(np.int64).sum()) > 4 * pool["capacity_entries"]
+    assert 0 < pool["high_water_entries"] <= pool["capacity_entries"]
+    for i in [0, 1, 5000, 16383]:
+        ref = oracle.run(W.C1, W.Policy(W.WAIT), [1], n_reps=1, rep_begin=i)
+        assert_rows_equal(rows[:, i:i + 1], ref, f"C1 rep {i}")
+
+
+def test_restart_pool_exhaustion_is_reported():
+    """A pool of one chunk cannot hold the concurrent restarts of 256 C1
+    replications: some rows report status 2, the others stay bit-exact."""
+    from paper_2504_11320_b200 import Scheduler
+    s = Scheduler(W.C1, W.Policy(W.WAIT), [1], restart_cap=64)
+    rows = s.run_host(W.C1.seed, 0, 256, W.C1.horizon_s)
+    s.close()
+    st = rows[oracle.F["status"]]
+    assert (st == 2).any() and set(st.tolist()) <= {0, 2}
+    ok = np.nonzero(st == 0)[0][:4].tolist()
+    for i in ok:
+        ref = oracle.run(W.C1, W.Policy(W.WAIT), [1], n_reps=1, rep_begin=i)
+        assert_rows_equal(rows[:, i:i + 1], ref, f"C1 rep {i}")
