@@ -22,6 +22,8 @@ using namespace waitsim;
 // one for the class-ring engine (sched_run of fixed-length WAIT / FCFS)
 struct LaunchCfg {
   bool ring = false;
+  bool seg = false;                          // NESTED segment engine (fallback: the member engine's safe launch)
+  uint32_t seg_cap = 0;                      // seg: resident array capacity (records)
   uint32_t Rc = 0, Rc_safe = 0;              // member: residents; ring: staging slots
   uint32_t spare = 0;                        // ring: victim slots beyond Rc (8, 32 when evictions are expected)
   uint32_t rcap[32] = {}, rcap_safe[32] = {};  // ring: per-class ring capacity
@@ -83,8 +85,11 @@ struct sched_s {
   size_t out_cap = 0;
   // launch: main (speculative capacity) and fallback (safe capacity) per engine
   int sm_count = 0;
-  LaunchCfg mem, rng;
+  LaunchCfg mem, rng, sg;
   bool use_ring = false;                     // sched_run uses the class-ring engine
+  bool use_seg = false;                      // sched_run / sched_run_trace use the segment engine
+  int64_t* d_seg_a = nullptr;                // segment engine: per-warp arrival-tick arrays
+  size_t seg_a_cap = 0;
   double n_star_c[32] = {};                  // fluid prompts in service per class
   double m_star = 0;                         // fluid KV occupancy M*
   double tv_peak = 1.0;                      // max time-varying rate / lambda (speculative sizing)
@@ -241,10 +246,29 @@ int prepare(sched_s* h) {
     } catch (...) {
     }
   }
+  // NESTED segment geometry (segment engine): entry stage b_k = e_{k-1}+1
+  // (b_0 = 0: the FIFO), W_k = e_k - b_k non-entry stages, histogram /
+  // cohort-ring offsets
+  if (h->in.policy == SCHED_NESTED) {
+    uint32_t ho = 0, co = 0;
+    for (size_t k = 0; k < h->in.seg_end.size() && k < 32; ++k) {
+      const uint32_t b = k ? h->in.seg_end[k - 1] + 1 : 0u, w = h->in.seg_end[k] - b;
+      h->base.seg_b[k] = b;
+      h->base.seg_w[k] = w;
+      h->base.hoff[k] = ho;
+      h->base.coff[k] = co;
+      ho += w;
+      co += w + 1;
+    }
+    h->base.hsize = ho;
+    h->base.csize = co;
+  }
   // choose warps per block maximising resident warps per SM
-  auto size_launch = [&](bool ring, uint32_t records, uint32_t* wsm, int* wpb_out, int* bps_out) -> int {
+  auto size_launch = [&](bool ring, uint32_t records, uint32_t* wsm, int* wpb_out, int* bps_out,
+                         uint32_t seg_cap = 0) -> int {
     *wsm = warp_smem_bytes(records, K, h->tv_any, ring, h->in.policy == SCHED_NESTED,
-                           h->in.policy == SCHED_WAIT ? (uint32_t)K : 1u);
+                           h->in.policy == SCHED_WAIT ? (uint32_t)K : 1u, seg_cap, h->base.hsize,
+                           h->base.csize);
     int best_w = 0;
     const int cands[] = {8, 4, 2, 1};
     for (int wpb : cands) {
@@ -253,7 +277,7 @@ int prepare(sched_s* h) {
       if (smem > (size_t)prop.sharedMemPerBlockOptin) continue;
       // max blocks per SM from shared memory and registers (occupancy API)
       int bps = 0;
-      const cudaError_t e = sim_occupancy(h->in.policy, 0, wpb * 32, smem, &bps, ring ? 1 : 0);
+      const cudaError_t e = sim_occupancy(h->in.policy, 0, wpb * 32, smem, &bps, seg_cap ? 2 : ring ? 1 : 0);
       if (e != cudaSuccess) return cuda_fail(e, "occupancy");
       if (bps * wpb > best_w) { best_w = bps * wpb; *wpb_out = wpb; *bps_out = bps; }
     }
@@ -378,6 +402,41 @@ int prepare(sched_s* h) {
     h->use_ring = L.grid > 0 && (forced || ((double)ring_rec <= 1.3 * (double)h->mem.Rc &&
                                             (in.policy == SCHED_WAIT || short_lp)));
   }
+  // segment engine (NESTED): O(entry-stage takes + admissions) per batch
+  // instead of a pass over every resident; replications
+  // that overflow its array re-run on the member engine's safe launch
+  h->use_seg = false;
+  if (h->in.policy == SCHED_NESTED && !(eng && std::string(eng) == "member")) {
+    LaunchCfg& L = h->sg;
+    L = LaunchCfg{};
+    L.seg = true;
+    L.Rc = L.Rc_safe = round32(h->in.thresholds[0]);  // staged admissions: n_1 per batch
+    double f = 1.5;
+    if (const char* fs = getenv("WAITSIM_SEG_CAP")) f = std::max(0.1, atof(fs));
+    // the member engine's speculative population (live residents) x f:
+    // room for the tombstones of mid-segment completions between compactions
+    L.seg_cap = round32((uint64_t)(f * h->mem.Rc) + 2ull * h->in.thresholds[0]);
+    int wpb = 1, bps = 0;
+    if (size_launch(false, L.Rc, &L.warp_smem, &wpb, &bps, L.seg_cap) == 0) {
+      L.wpb = wpb;
+      L.blocks_per_sm = bps;
+      L.block = wpb * 32;
+      L.grid = h->sm_count * bps;
+      L.fallback = true;  // the member engine's safe launch
+      h->use_seg = true;
+    } else if (eng && std::string(eng) == "seg") {
+      return SCHED_E_INVALID;
+    }
+    if (h->use_seg) {
+      const size_t need = (size_t)L.grid * L.wpb * L.seg_cap;
+      if (need > h->seg_a_cap) {
+        cudaFree(h->d_seg_a);
+        h->d_seg_a = nullptr;
+        CK(cudaMalloc(&h->d_seg_a, need * 8));
+        h->seg_a_cap = need;
+      }
+    }
+  }
   const int n_rings = h->in.policy == SCHED_WAIT ? K : 1;
   if (!h->d_pool_a) {
     // one pool of restart-FIFO chunks for every replication of a launch:
@@ -415,6 +474,7 @@ int prepare(sched_s* h) {
 // capacities of one launch of configuration L (safe = the fallback launch)
 void set_caps(DevParams& p, const LaunchCfg& L, bool safe, int K) {
   p.ring_engine = L.ring ? 1u : 0u;
+  p.seg_engine = 0;
   p.spare = L.spare;
   p.Rc = safe ? L.Rc_safe : L.Rc;
   p.warp_smem = safe ? L.fb_warp_smem : L.warp_smem;
@@ -428,6 +488,45 @@ void set_caps(DevParams& p, const LaunchCfg& L, bool safe, int K) {
 
 int launch(sched_s* h, DevParams p, cudaStream_t st, const LaunchCfg& L) {
   const int K = p.K;
+  if (L.seg) {
+    // segment engine; replications that overflow its array re-run on the
+    // member engine with the safe capacity
+    CK(cudaMemsetAsync(h->d_counter, 0, 16, st));
+    if (p.n_reps > h->retry_cap) {
+      cudaFree(h->d_retry);
+      h->d_retry = nullptr;
+      CK(cudaMalloc(&h->d_retry, (size_t)p.n_reps * 4));
+      h->retry_cap = p.n_reps;
+    }
+    DevParams q = p;
+    q.work_counter = h->d_counter;
+    q.retry_count = h->d_counter + 2;
+    q.retry_list = h->d_retry;
+    q.fallback = 0;
+    q.ring_engine = 0;
+    q.seg_engine = 1;
+    q.seg_cap = L.seg_cap;
+    q.seg_a = h->d_seg_a;
+    q.Rc = L.Rc;
+    q.warp_smem = L.warp_smem;
+    int grid = L.grid;
+    if ((int64_t)p.n_reps < (int64_t)grid * L.wpb) grid = std::max<int>(1, (int)((p.n_reps + L.wpb - 1) / L.wpb));
+    CK(launch_sim(q, grid, L.block, (size_t)L.wpb * L.warp_smem, st));
+    const LaunchCfg& M = h->mem;
+    DevParams f = p;
+    f.seg_engine = 0;
+    f.seg_cap = 0;
+    f.fallback = 1;
+    f.work_counter = h->d_counter + 1;
+    f.retry_count = h->d_counter + 2;
+    f.retry_list = h->d_retry;
+    set_caps(f, M, M.fallback, K);
+    const int fwpb = M.fallback ? M.fb_wpb : M.wpb, fblock = M.fallback ? M.fb_block : M.block;
+    const int fmax = M.fallback ? M.fb_grid : M.grid;
+    const int fgrid = std::min(fmax, std::max(1, (int)((p.n_reps + fwpb - 1) / fwpb)));
+    CK(launch_sim(f, fgrid, fblock, (size_t)fwpb * f.warp_smem, st));
+    return 0;
+  }
   CK(cudaMemsetAsync(h->d_counter, 0, 16, st));
   p.work_counter = h->d_counter;
   p.retry_count = h->d_counter + 2;
@@ -686,7 +785,7 @@ int sched_run(sched_t h, uint64_t seed, uint64_t rep_begin, uint32_t n_reps, dou
   p.T_t = std::llround(horizon_s * 1e12);
   p.trace_mode = 0;
   p.out = out_dev;
-  return launch(h, p, (cudaStream_t)cuda_stream, h->use_ring ? h->rng : h->mem);
+  return launch(h, p, (cudaStream_t)cuda_stream, h->use_seg ? h->sg : h->use_ring ? h->rng : h->mem);
 }
 
 int sched_run_host(sched_t h, uint64_t seed, uint64_t rep_begin, uint32_t n_reps,
@@ -765,7 +864,7 @@ int sched_run_trace(sched_t h, const int64_t* t_ticks, const int32_t* cls, const
     p.log = d_log;
     p.log_cap = log_host ? log_cap : 0;
     p.log_n = d_logn;
-    rc = launch(h, p, 0, h->mem);
+    rc = launch(h, p, 0, h->use_seg ? h->sg : h->mem);
     if (rc == 0) {
       e = cudaDeviceSynchronize();
       if (e == cudaSuccess) e = cudaMemcpy(out_host, d_out, out_bytes, cudaMemcpyDeviceToHost);
@@ -789,8 +888,8 @@ int sched_get_launch_info(sched_t h, sched_launch_info* out) {
   if (int rc = prepare(h)) return rc;
   // the configuration sched_run uses (class-ring engine when eligible);
   // capacities in resident records (ring engine: rings + staging slots)
-  const LaunchCfg& L = h->use_ring ? h->rng : h->mem;
-  uint32_t spec = L.Rc, safe = L.Rc_safe;
+  const LaunchCfg& L = h->use_seg ? h->sg : h->use_ring ? h->rng : h->mem;
+  uint32_t spec = L.seg ? L.seg_cap : L.Rc, safe = L.seg ? h->mem.Rc_safe : L.Rc_safe;
   for (int c = 0; L.ring && c < (int)h->in.lambda.size(); ++c) { spec += L.rcap[c]; safe += L.rcap_safe[c]; }
   out->grid = L.grid;
   out->block = L.block;
@@ -801,9 +900,9 @@ int sched_get_launch_info(sched_t h, sched_launch_info* out) {
   out->max_resident = (int32_t)safe;
   out->restart_cap = (int32_t)std::min<uint64_t>(h->pool_entries, INT32_MAX);
   out->spec_resident = (int32_t)spec;
-  out->fallback_grid = L.fallback ? L.fb_grid : 0;
-  out->fallback_warps_per_block = L.fallback ? L.fb_wpb : 0;
-  out->engine = L.ring ? 1 : 0;
+  out->fallback_grid = L.seg ? (h->mem.fallback ? h->mem.fb_grid : h->mem.grid) : L.fallback ? L.fb_grid : 0;
+  out->fallback_warps_per_block = L.seg ? (h->mem.fallback ? h->mem.fb_wpb : h->mem.wpb) : L.fallback ? L.fb_wpb : 0;
+  out->engine = L.seg ? 2 : L.ring ? 1 : 0;
   return SCHED_OK;
 }
 
@@ -874,6 +973,7 @@ void sched_destroy(sched_t h) {
   cudaFree(h->d_cdf_guide);
   cudaFree(h->d_stage_info);
   cudaFree(h->d_pool_a);
+  cudaFree(h->d_seg_a);
   cudaFree(h->d_pool_e);
   cudaFree(h->d_pool_llp);
   cudaFree(h->d_pool_next);

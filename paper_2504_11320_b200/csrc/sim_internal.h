@@ -39,6 +39,17 @@ struct DevParams {
   uint32_t rcap[kMaxClasses];      // ring capacity (records) of class c
   uint32_t roff[kMaxClasses];      // first record of ring c after the staging area
   uint32_t fl[kMaxClasses];        // fixed l | l' << 16 of class c
+  // segment engine (NESTED): residents in one admission-
+  // ordered array that is sorted by stage, segment k a contiguous range;
+  // per segment the entry stage b_k = e_{k-1}+1 (b_0 = 0: the FIFO) and the
+  // number of non-entry stages W_k = e_k - b_k; completion histograms
+  // (W_k buckets from hoff[k]) and cohort rings (W_k+1 slots from coff[k])
+  uint32_t seg_engine;
+  uint32_t seg_cap;                // resident array capacity (records)
+  uint32_t seg_b[kMaxSegments], seg_w[kMaxSegments];
+  uint32_t hoff[kMaxSegments], coff[kMaxSegments];
+  uint32_t hsize, csize;           // total buckets / cohort slots
+  int64_t* seg_a;                  // [warps of the launch][seg_cap] arrival ticks of the residents (device)
   uint32_t warp_smem;      // bytes of shared memory per warp
   uint64_t seed;
   uint64_t rep_begin;      // global index of local replication 0
@@ -88,8 +99,13 @@ struct DevParams {
 
 // shared-memory bytes per warp for a given resident capacity / class count
 inline uint32_t warp_smem_bytes(uint32_t Rc, int K, bool tv = false, bool ring = false, bool nested = false,
-                                uint32_t n_rings = 1) {
+                                uint32_t n_rings = 1, uint32_t seg_cap = 0, uint32_t hsize = 0,
+                                uint32_t csize = 0) {
   uint32_t b = Rc * 16u;                    // residents: a (i64) + packed (l, l', s, meta)
+  // segment engine: staging (Rc) + resident array (8 B records; arrival
+  // ticks in global memory) + histograms (3 x u32 per bucket) + cohort rings
+  // (2 x u32 per slot) + eviction scratch
+  if (seg_cap) b += seg_cap * 8u + ((hsize * 12u + csize * 8u + 15u) & ~15u) + 256u;
   b += (uint32_t)K * (32u * 12u);           // generated windows (t, l, l')
   b += (uint32_t)K * (32u * 12u);           // private admission windows (t, l, l')
   b += 32u * 8u;                            // staged restart ticks
@@ -99,7 +115,7 @@ inline uint32_t warp_smem_bytes(uint32_t Rc, int K, bool tv = false, bool ring =
   if (nested) b += ((Rc + 31u) / 32u + 15u) & ~15u;  // per-chunk activity summaries
   if (tv) b += (uint32_t)K * (32u * 16u);   // operational-time windows (generated, private)
   b = (b + 15u) & ~15u;
-  b += (n_rings * 12u + 15u) & ~15u;        // restart FIFO chunk cursors (head, head index, tail)
+  b += n_rings * 32u;                        // restart FIFO chunk cursors (head, head index, tail, tail index) + chunk stash
   return b;
 }
 

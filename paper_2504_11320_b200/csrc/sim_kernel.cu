@@ -131,6 +131,16 @@ __device__ __forceinline__ u128 warp_sum_u128(u128 x) {
   }
   return x;
 }
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t x) {
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) x += __shfl_xor_sync(FULL, x, d);
+  return x;
+}
+__device__ __forceinline__ int64_t warp_sum_i64(int64_t x) {
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) x += __shfl_xor_sync(FULL, x, d);
+  return x;
+}
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -168,6 +178,15 @@ struct __align__(16) RRec {
   uint32_t seq;
 };
 constexpr uint32_t XF_FT = 0x80000000u, XF_PEND = 0x40000000u, XF_X = 0x3FFFFFFFu;
+// segment-engine resident (NESTED), shared memory: l | l' << 16,
+// cohort clock x (bits 0-30: the segment clock at which it ran its entry
+// stage; stage = b_k + C_k - x) | first token emitted before a restart (bit
+// 31); its arrival tick sits at the same position of a per-warp global array
+struct __align__(8) SRec {
+  uint32_t llp;
+  uint32_t xf;
+};
+constexpr uint32_t SX_FT = 0x80000000u, SX_X = 0x7FFFFFFFu;
 __device__ __forceinline__ uint32_t wrap(uint32_t p, uint32_t cap) { return p >= cap ? p - cap : p; }  // staging mark: came from a restart ring
 
 // # of leading entries of the sorted array v[0..n) that precede `key`
@@ -190,7 +209,9 @@ struct __align__(16) WarpStats {
   uint64_t arrivals, admitted, completed, completed_after_T, completed_tokens, first_tokens,
       batches, request_steps, prefill_steps, evictions, cbi, sum_waiting, h;
   int64_t busy, idle, max_kv, log_n;
+  u128 acc_adm, acc_ev;                 // segment engine: admitted / evicted arrival-tick sums
 };
+static_assert(sizeof(WarpStats) <= 256, "WarpStats slot");
 
 // arrival tick at operational time tau of a time-varying class: invert the
 // integrated piecewise-constant rate
@@ -270,7 +291,7 @@ __device__ __forceinline__ void gen_window(GEN_WINDOW_ARGS) {
   else gen_window_call(GEN_WINDOW_PASS);
 }
 
-template <int POL, bool TRACE, bool RING>
+template <int POL, bool TRACE, bool RING, bool SEG>
 struct WarpSim {
   const DevParams& P;
   const int lane;
@@ -289,7 +310,15 @@ struct WarpSim {
   WarpStats* st;                     // metric accumulators
   uint64_t* xs;                      // [32] RING eviction scratch (per-class sums)
   uint8_t* csum;                     // NESTED: per-chunk lowest resident segment
-  uint32_t* rq;                      // [n_rings][4] restart FIFO chunks: head, head index, tail, tail index
+  uint32_t* rq;                      // [n_rings][8] restart FIFO chunks: head, head index, tail, tail index, stash
+  // SEG (NESTED segment engine): residents in one array in
+  // admission order = stage order; segment k is the range [P_k, P_{k-1})
+  // (k = 0: [P_0, tail)), non-entry part [P_k, E_k), entry-stage part
+  // [E_k, P_{k-1}); completed records stay as tombstones until compaction
+  SRec* sa;                          // [seg_cap] positions [head, tail)
+  int64_t* ga;                       // [seg_cap] their arrival ticks (global memory, this warp's slot)
+  uint32_t* hcnt; uint32_t* hsll; uint32_t* hslp;  // [hsize] completion histograms: count, sum (l+l'), sum l'
+  uint32_t* con; uint32_t* col;      // [csize] cohort rings: records | exiting << 16, sum l of the exiting
 
   // per-class cursor state, lane c holds class c (and ring c for WAIT; ring 0
   // otherwise).  The generated window [vbase, vbase+32) serves visibility
@@ -312,6 +341,16 @@ struct WarpSim {
   // cnt[32 + c], arrival-tick sum in psum()[c] (the NESTED rank / snap slots)
   __device__ __forceinline__ uint64_t* psum() const { return (uint64_t*)rank; }
 
+  // SEG, lane k = segment k: range starts P_k / E_k, clock C_k (batches the
+  // segment took part in), C_k mod W_k, C_k mod (W_k + 1), alive non-entry /
+  // entry-stage residents, T_k = sum over alive non-entry (l - x)
+  uint32_t g_P, g_E, g_C, g_R, g_Rc, g_nne, g_nen;
+  int64_t g_T;
+  uint32_t head, tail;               // uniform
+  uint32_t pf_n;                     // uniform: first tokens due at the next batch (stage 1) ...
+  uint64_t pf_a;                     // ... and their arrival-tick sum
+  uint64_t acc_adm, acc_ev;          // lane-local arrival-tick sums of admissions / evictions
+
   // replication
   uint32_t rep, rglob;
   int64_t now, KV;
@@ -325,13 +364,23 @@ struct WarpSim {
   uint32_t n_plan_res;
   bool below;         // no batch because of the threshold test (idle skip allowed)
 
-  __device__ WarpSim(const DevParams& p, unsigned char* base, int lane_)
+  __device__ WarpSim(const DevParams& p, unsigned char* base, int lane_, uint32_t slot)
       : P(p), lane(lane_) {
     const uint32_t Rc = p.Rc;
     rr = (Rec*)base;
     // RING: 32 spare staging slots hold the victims of one eviction round
     rg = (RRec*)(rr + Rc + (RING ? p.spare : 0u));
     vt = (int64_t*)(rr + Rc + (RING ? p.spare + p.roff[p.K - 1] + p.rcap[p.K - 1] : 0u));
+    if (SEG) {
+      ga = p.seg_a + (size_t)slot * p.seg_cap;
+      sa = (SRec*)(rr + Rc);
+      hcnt = (uint32_t*)(sa + p.seg_cap);
+      hsll = hcnt + p.hsize;
+      hslp = hsll + p.hsize;
+      con = hslp + p.hsize;
+      col = con + p.csize;
+      vt = (int64_t*)((unsigned char*)hcnt + ((p.hsize * 12u + p.csize * 8u + 15u) & ~15u));
+    }
     at = vt + p.K * 32;
     re = at + p.K * 32;
     // l / l' of both windows share one offset space with the ticks:
@@ -345,31 +394,46 @@ struct WarpSim {
     snap = rank + 32;
     st = (WarpStats*)(snap + 32);
     xs = (uint64_t*)((unsigned char*)st + 256);
-    csum = (uint8_t*)st + (RING ? 512 : 256);  // NESTED: (Rc + 31) / 32 chunk summaries
-    vtau = (int64_t*)((unsigned char*)st + (RING ? 512 : 256) +
+    csum = (uint8_t*)st + ((RING || SEG) ? 512 : 256);  // NESTED: (Rc + 31) / 32 chunk summaries
+    vtau = (int64_t*)((unsigned char*)st + ((RING || SEG) ? 512 : 256) +
                       (POL == SCHED_NESTED ? (((p.Rc + 31) / 32 + 15) & ~15u) : 0u));
     atau = vtau + p.K * 32;
-    rq = (uint32_t*)(base + p.warp_smem - ((p.n_rings * 12u + 15u) & ~15u));
+    rq = (uint32_t*)(base + p.warp_smem - p.n_rings * 32u);
+    if (lane < p.n_rings) rq[8 * lane + 4] = 0;  // empty chunk stash
   }
 
   __device__ void flush_acc() {
     const u128 a = warp_sum_u128(acc_arr), b = warp_sum_u128(acc_done_a), c = warp_sum_u128(acc_ft_a);
     if (lane == 0) { st->acc_arr += a; st->acc_done_a += b; st->acc_ft_a += c; }
     acc_arr = acc_done_a = acc_ft_a = 0;
+    if (SEG) {
+      const u128 d = warp_sum_u128(acc_adm), e = warp_sum_u128(acc_ev);
+      if (lane == 0) { st->acc_adm += d; st->acc_ev += e; }
+      acc_adm = acc_ev = 0;
+    }
   }
   __device__ __forceinline__ void maybe_flush() {
-    if (__any_sync(FULL, ((acc_arr | acc_done_a | acc_ft_a) >> 60) != 0)) flush_acc();
+    uint64_t m = acc_arr | acc_done_a | acc_ft_a;
+    if (SEG) m |= acc_adm | acc_ev;
+    if (__any_sync(FULL, (m >> 60) != 0)) flush_acc();
   }
 
   // ------------------------------------------- restart FIFOs (chunk pool)
   // FIFO q holds positions [rhead, rtail) (lane q's counters) in a linked
-  // list of kRestartChunk-entry chunks: rq[4q] = chunk of position
-  // rhead (index rq[4q+1] = its position / kRestartChunk), rq[4q+2] = chunk
-  // of the next write position rtail (index rq[4q+3]).  Chunks come from the
-  // device-wide pool: a lock-free free stack (ABA tag in the high word), else
-  // never-used chunks; a chunk is returned when the committed head passes it
-  // and at the end of the replication.
-  __device__ uint32_t pool_alloc() const {
+  // list of kRestartChunk-entry chunks: rq[8q] = chunk of position
+  // rhead (index rq[8q+1] = its position / kRestartChunk), rq[8q+2] = chunk
+  // of the next write position rtail (index rq[8q+3]).  Chunks come from a
+  // per-FIFO stash of up to kStash free chunks (rq[8q+4] = count, rq[8q+5..]
+  // = chunks; kept across this warp's replications, returned at kernel
+  // exit), else the device-wide pool: a lock-free free stack (ABA tag in the
+  // high word), else never-used chunks.  The stash keeps the global free
+  // stack -- one hot word -- off the path of eviction-heavy runs (C5: a
+  // chunk every few batches per warp).  A chunk is returned when the
+  // committed head passes it and at the end of the replication.
+  static constexpr uint32_t kStash = 3;
+  __device__ uint32_t pool_alloc(int q) const {
+    const uint32_t n = rq[8 * q + 4];
+    if (n) { rq[8 * q + 4] = n - 1; return rq[8 * q + 4 + n]; }
     unsigned long long old = atomicAdd(P.pool_free, 0ull);
     while ((uint32_t)old != kNoChunk) {
       const uint32_t nxt = __ldcg(P.pool_next + (uint32_t)old);
@@ -381,7 +445,12 @@ struct WarpSim {
     const uint32_t c = atomicAdd(P.pool_bump, 1u);
     return c < P.pool_chunks ? c : kNoChunk;
   }
-  __device__ void pool_release(uint32_t c) const {
+  __device__ void pool_release(int q, uint32_t c) const {
+    const uint32_t n = rq[8 * q + 4];
+    if (n < kStash) { rq[8 * q + 5 + n] = c; rq[8 * q + 4] = n + 1; return; }
+    pool_push(c);
+  }
+  __device__ void pool_push(uint32_t c) const {
     unsigned long long old = atomicAdd(P.pool_free, 0ull);
     for (;;) {
       __stcg(P.pool_next + c, (uint32_t)old);
@@ -394,60 +463,65 @@ struct WarpSim {
   }
   // pool entry of position pos (>= the committed head) of FIFO q
   __device__ __forceinline__ size_t fifo_entry(int q, uint32_t pos) const {
-    uint32_t c = rq[4 * q], ci = rq[4 * q + 1];
+    uint32_t c = rq[8 * q], ci = rq[8 * q + 1];
     for (const uint32_t want = pos / kRestartChunk; ci < want; ++ci) c = __ldcg(P.pool_next + c);
     return (size_t)c * kRestartChunk + pos % kRestartChunk;
   }
   // pool entry of tail position pos (the tail chunk or the one after it)
   __device__ __forceinline__ size_t fifo_wentry(int q, uint32_t pos) const {
-    uint32_t c = rq[4 * q + 2];
-    if (pos / kRestartChunk != rq[4 * q + 3]) c = __ldcg(P.pool_next + c);
+    uint32_t c = rq[8 * q + 2];
+    if (pos / kRestartChunk != rq[8 * q + 3]) c = __ldcg(P.pool_next + c);
     return (size_t)c * kRestartChunk + pos % kRestartChunk;
   }
   // lane q: chunks for cnt (<= 32) more entries at the tail t of FIFO q
   // (the chunk of the next write position included); false: pool exhausted
   __device__ bool fifo_reserve(int q, uint32_t t, uint32_t cnt) const {
-    if (rq[4 * q + 2] == kNoChunk) {
-      const uint32_t c = pool_alloc();
+    if (rq[8 * q + 2] == kNoChunk) {
+      const uint32_t c = pool_alloc(q);
       if (c == kNoChunk) return false;
-      rq[4 * q] = rq[4 * q + 2] = c;
-      rq[4 * q + 1] = rq[4 * q + 3] = t / kRestartChunk;
+      rq[8 * q] = rq[8 * q + 2] = c;
+      rq[8 * q + 1] = rq[8 * q + 3] = t / kRestartChunk;
     }
-    if ((t + cnt) / kRestartChunk > rq[4 * q + 3]) {
-      const uint32_t c = pool_alloc();
+    if ((t + cnt) / kRestartChunk > rq[8 * q + 3]) {
+      const uint32_t c = pool_alloc(q);
       if (c == kNoChunk) return false;
-      __stcg(P.pool_next + rq[4 * q + 2], c);
+      __stcg(P.pool_next + rq[8 * q + 2], c);
     }
     return true;
   }
   // lane q, after the writes: the tail chunk follows the new tail position
   __device__ void fifo_tail_done(int q, uint32_t t_new) const {
-    if (t_new / kRestartChunk > rq[4 * q + 3]) {
-      rq[4 * q + 2] = __ldcg(P.pool_next + rq[4 * q + 2]);
-      rq[4 * q + 3] += 1;
+    if (t_new / kRestartChunk > rq[8 * q + 3]) {
+      rq[8 * q + 2] = __ldcg(P.pool_next + rq[8 * q + 2]);
+      rq[8 * q + 3] += 1;
     }
   }
   // lane q: return the chunks the committed head has passed
   __device__ void fifo_commit(int q, uint32_t head) const {
-    while (rq[4 * q + 2] != kNoChunk && rq[4 * q + 1] < head / kRestartChunk) {
-      const uint32_t c = rq[4 * q];
-      rq[4 * q] = __ldcg(P.pool_next + c);
-      rq[4 * q + 1] += 1;
-      pool_release(c);
+    while (rq[8 * q + 2] != kNoChunk && rq[8 * q + 1] < head / kRestartChunk) {
+      const uint32_t c = rq[8 * q];
+      rq[8 * q] = __ldcg(P.pool_next + c);
+      rq[8 * q + 1] += 1;
+      pool_release(q, c);
     }
+  }
+  // lanes < n_rings: return the stashed chunks to the pool (kernel exit)
+  __device__ void flush_stash() const {
+    if (lane < P.n_rings)
+      for (uint32_t i = 0; i < rq[8 * lane + 4]; ++i) pool_push(rq[8 * lane + 5 + i]);
   }
   // lane q: return every chunk of FIFO q (end of the replication)
   __device__ void fifo_release_all(int q) const {
-    if (rq[4 * q + 2] == kNoChunk) return;
-    uint32_t c = rq[4 * q];
+    if (rq[8 * q + 2] == kNoChunk) return;
+    uint32_t c = rq[8 * q];
     for (;;) {
       const uint32_t nxt = __ldcg(P.pool_next + c);
-      const bool last = c == rq[4 * q + 2];
-      pool_release(c);
+      const bool last = c == rq[8 * q + 2];
+      pool_release(q, c);
       if (last) break;
       c = nxt;
     }
-    rq[4 * q] = rq[4 * q + 2] = kNoChunk;
+    rq[8 * q] = rq[8 * q + 2] = kNoChunk;
   }
   // NESTED stage info: segment index (bits 0-5), last stage of the segment
   // (bit 6), entry stage (bit 7); counter slot = segment (+32 at entry)
@@ -625,7 +699,7 @@ struct WarpSim {
   // windows); FCFS additionally cuts at the first prompt failing the
   // admission test (reading R15).
   // first staging slot: after the residents (member engine) or 0 (RING)
-  __device__ __forceinline__ uint32_t sbase() const { return RING ? 0u : n_res; }
+  __device__ __forceinline__ uint32_t sbase() const { return (RING || SEG) ? 0u : n_res; }
 
   // FCFS admission cut: lane i holds staged candidate i (prefill length l);
   // the longest prefix passing the test of PAPER.md:1427, 1745 (R15)
@@ -1051,14 +1125,15 @@ struct WarpSim {
       // Algorithm 2: largest k with Q_{k',entry} >= n_k' for all k' <= k
       // (PAPER.md:1640); batch min{n_k, Q_{k,s}} per stage (line 1642)
       if (waiting_total() < P.thr[0]) { below = true; return false; }
-      const bool pass = lane >= 1 && lane < P.n_seg && cnt[32 + lane] >= P.thr[lane];
+      const uint32_t q_entry = SEG ? g_nen : cnt[32 + lane];  // residents waiting at segment lane's entry stage
+      const bool pass = lane >= 1 && lane < P.n_seg && q_entry >= P.thr[lane];
       const uint32_t fail = ~__ballot_sync(FULL, pass) & ~1u;  // bit 0 = segment 1 (passed)
       const int ks = min(__ffs(fail) - 2, P.n_seg - 1);
       kstar = ks;
       uint32_t npr = 0;
       if (lane <= ks) {
-        npr = cnt[lane];
-        if (lane >= 1) npr += min(cnt[32 + lane], P.thr[lane]);
+        npr = SEG ? g_nne : cnt[lane];
+        if (lane >= 1) npr += min(q_entry, P.thr[lane]);
       }
       n_plan_res = __reduce_add_sync(FULL, npr);
       save_cursors();
@@ -1288,6 +1363,404 @@ struct WarpSim {
     peak = P.M + excess;
   }
 
+
+  // ====================================== S4/S5, NESTED segment engine (SEG)
+  // Every prompt passes the stages in admission order: an entry stage takes
+  // its oldest n_k first (reading R6) and every non-entry
+  // stage of an active segment advances (P14), so the resident array in
+  // admission order is sorted by stage and segment k is a contiguous range
+  // (DESIGN.md §5.2).  A non-entry member of segment k that ran the entry
+  // stage b_k at clock x (C_k = batches segment k took part in) is at stage
+  // b_k + C_k - x.  Members that complete inside the segment are counted in
+  // a histogram keyed by their completion clock x + l' - b_k; members that
+  // reach e_k alive are counted per cohort x and leave as one block (the
+  // range boundary moves).  A batch therefore touches the records of the
+  // entry-stage takes and of the admissions only; completed records stay
+  // as tombstones until the array is compacted.
+  __device__ __forceinline__ static uint32_t wrapc(uint32_t v, uint32_t n) { return v >= n ? v - n : v; }
+
+  // segment of position p in [head, tail): k = #{j : P_j > p}; entry stage
+  // iff k >= 1 and p >= E_k (every lane runs the shuffles)
+  __device__ __forceinline__ int seg_of(uint32_t p, bool& entry) const {
+    int k = 0;
+    for (int j = 0; j < P.n_seg; ++j) k += bcast32(g_P, j) > p;
+    const uint32_t Ek = __shfl_sync(FULL, g_E, k & 31);
+    entry = k >= 1 && p >= Ek;
+    return k;
+  }
+  // cohort-ring slot of clock x in segment k (Rc = C_k mod (W_k + 1), C_k - x <= W_k)
+  __device__ __forceinline__ uint32_t coh_slot(uint32_t k, uint32_t Rc, uint32_t C, uint32_t x) const {
+    const uint32_t d = C - x;
+    return P.coff[k] + (Rc >= d ? Rc - d : Rc + P.seg_w[k] + 1u - d);
+  }
+
+  // S4, LIFO eviction from the array tail: up to 32
+  // records per round, newest first; a record's freed KV is l + s - 1 (+1
+  // if it is in the plan: non-entry stages of active segments, and the
+  // oldest n_k alive at an active entry stage)
+  __device__ void seg_memory(uint32_t& n_evict, int64_t& peak) {
+    peak = KV + (int64_t)n_plan_res + sum_new_l;
+    if (peak <= P.M) return;
+    int64_t excess = peak - P.M;
+    const uint32_t nen0 = g_nen;   // lane k: alive entry-stage residents at decision time
+    uint32_t seen = 0;             // lane k: of which evicted so far
+    while (excess > 0 && n_res > 0 && tail > head) {
+      const uint32_t span = tail - head;
+      const bool v = (uint32_t)lane < span;
+      const uint32_t p = tail - 1 - (uint32_t)lane;  // lane 0 = the newest record
+      SRec r = {0, 0};
+      int64_t a = 0;
+      if (v) { r = sa[p]; a = ga[p]; }
+      bool en = false;
+      int k = 0;
+      // (the usual case: the whole chunk lies in segment 1's range)
+      if (tail - min(span, 32u) < bcast32(g_P, 0)) k = seg_of(v ? p : tail - 1, en);
+      const uint32_t kk = (uint32_t)k & 31u;
+      const uint32_t l = r.llp & 0xFFFFu, lp = r.llp >> 16, x = r.xf & SX_X;
+      const uint32_t Ck = __shfl_sync(FULL, g_C, kk), Rk = __shfl_sync(FULL, g_R, kk);
+      const uint32_t Rck = __shfl_sync(FULL, g_Rc, kk);
+      const uint32_t seen_k = __shfl_sync(FULL, seen, kk), nen_k = __shfl_sync(FULL, nen0, kk);
+      const uint32_t bk = P.seg_b[kk], Wk = P.seg_w[kk];
+      const uint32_t s = en ? bk : bk + Ck - x;  // next stage to run
+      const bool alive = v && (en ? lp >= bk : s <= lp);
+      const bool ea = alive && en;
+      const uint32_t grp = __match_any_sync(FULL, ea ? kk : 0x100u + (uint32_t)lane);
+      uint32_t inp = 0;
+      if (alive && k <= kstar) {
+        if (!en) inp = 1u;
+        else inp = nen_k - 1u - (seen_k + __popc(grp & lanemask_lt())) < P.thr[kk];  // rank from the head
+      }
+      const uint32_t f = alive ? l + s - 1 + inp : 0u;
+      const uint32_t cum = warp_incl_scan_u32(f, lane);
+      const uint32_t hit = __ballot_sync(FULL, alive && (int64_t)cum >= excess);
+      const uint32_t ntr = hit ? (uint32_t)__ffs(hit) : min(span, 32u);  // records removed from the tail
+      const bool tr = (uint32_t)lane < ntr;
+      const bool ev = tr && alive;
+      const uint32_t evm = __ballot_sync(FULL, ev);
+      const uint32_t ne = __popc(evm);
+      const uint32_t before = __popc(evm & lanemask_lt());
+      const uint32_t tail_q = __shfl_sync(FULL, rtail, 0);
+      const uint32_t my_cnt = lane == 0 ? ne : 0u;
+      const bool res_ok = my_cnt == 0 || fifo_reserve(lane, rtail, my_cnt);
+      if (__any_sync(FULL, !res_ok)) { status = 2; return; }
+      cnt[lane] = 0;
+      cnt[32 + lane] = 0;
+      xs[lane] = 0;
+      __syncwarp();
+      if (ev) {  // restart record, in eviction order (re-enter the queue)
+        const size_t e = fifo_wentry(0, tail_q + before);
+        const bool emitted = (r.xf & SX_FT) || s >= 2;
+        P.pool_a[e] = a;
+        P.pool_e[e] = now;
+        P.pool_llp[e] = l | (lp << 16) | (emitted ? 0x80000000u : 0u);
+        acc_ev += (uint64_t)a;
+        if (en) {
+          sh_add_u32(&cnt[32 + kk], 1u);
+        } else {
+          sh_add_u32(&cnt[kk], 1u);
+          sh_add_u64(&xs[kk], (uint64_t)((int64_t)l - (int64_t)x));
+        }
+      }
+      if (tr && !en) {  // the record leaves its cohort, and its pending completion or exit
+        const uint32_t ci = coh_slot(kk, Rck, Ck, x);
+        const bool exits = lp > bk + Wk;
+        sh_add_u32(&con[ci], (ev && exits) ? ~0x10000u : ~0u);  // -(1 + (1 << 16)) / -1
+        if (ev && exits) sh_add_u32(&col[ci], 0u - l);
+        if (ev && !exits) {  // completion due at clock x + l' - b_k >= C_k
+          const uint32_t i = P.hoff[kk] + wrapc(Rk + (x + lp - bk - Ck), Wk);
+          sh_add_u32(&hcnt[i], ~0u);
+          sh_add_u32(&hsll[i], 0u - (l + lp));
+          sh_add_u32(&hslp[i], 0u - lp);
+        }
+      }
+      // a first token due at the next batch (stage 1) is not emitted
+      const bool pf = ev && !en && k == 0 && s == 1 && !(r.xf & SX_FT);
+      pf_n -= __popc(__ballot_sync(FULL, pf));
+      pf_a -= warp_sum_u64(pf ? (uint64_t)a : 0ull);
+      __syncwarp();
+      if (lane < P.n_seg) {
+        g_nne -= cnt[lane];
+        g_T -= (int64_t)xs[lane];
+        g_nen -= cnt[32 + lane];
+        seen += cnt[32 + lane];
+      }
+      if (my_cnt) { rtail += my_cnt; fifo_tail_done(lane, rtail); }
+      if (lane == 0) st->evictions += ne;
+      excess -= (int64_t)__reduce_add_sync(FULL, ev ? f : 0u);
+      KV -= (int64_t)__reduce_add_sync(FULL, ev ? (l + s - 1) : 0u);
+      n_plan_res -= __reduce_add_sync(FULL, ev ? inp : 0u);
+      n_res -= ne;
+      n_evict += ne;
+      tail -= ntr;
+      g_P = min(g_P, tail);
+      g_E = min(g_E, tail);
+      __syncwarp();
+    }
+    if (excess > 0) drop_admissions(excess);
+    peak = P.M + excess;
+  }
+
+  // drop the tombstones of [head, tail) and move the rest to position 0
+  // (when an admission would pass the capacity); cohort record counts and
+  // range starts are recomputed
+  __device__ void seg_compact() {
+    const int L = P.n_seg;
+    for (uint32_t i = lane; i < P.csize; i += 32) con[i] &= 0xFFFF0000u;
+    __syncwarp();
+    uint32_t wp = 0, nP = 0xFFFFFFFFu, nE = 0xFFFFFFFFu;
+    for (uint32_t p0 = head; p0 < tail; p0 += 32) {
+      const uint32_t p = p0 + (uint32_t)lane;
+      const bool v = p < tail;
+      SRec r = {0, 0};
+      int64_t a = 0;
+      if (v) { r = sa[p]; a = ga[p]; }
+      bool en;
+      const int k = seg_of(v ? p : p0, en);
+      const uint32_t kk = (uint32_t)k & 31u;
+      const uint32_t lp = r.llp >> 16, x = r.xf & SX_X;
+      const uint32_t Ck = __shfl_sync(FULL, g_C, kk), Rck = __shfl_sync(FULL, g_Rc, kk);
+      const uint32_t bk = P.seg_b[kk];
+      const bool keep = v && (en ? lp >= bk : bk + Ck - x <= lp);
+      const uint32_t km = __ballot_sync(FULL, keep);
+      if (lane < L) {
+        if (nP == 0xFFFFFFFFu && g_P < p0 + 32) nP = wp + __popc(km & ((1u << (g_P - p0)) - 1u));
+        if (nE == 0xFFFFFFFFu && g_E < p0 + 32) nE = wp + __popc(km & ((1u << (g_E - p0)) - 1u));
+      }
+      if (keep) {
+        const uint32_t d = wp + __popc(km & lanemask_lt());
+        sa[d] = r;
+        ga[d] = a;
+        if (!en) sh_add_u32(&con[coh_slot(kk, Rck, Ck, x)], 1u);
+      }
+      wp += __popc(km);
+    }
+    if (lane < L) {
+      g_P = nP == 0xFFFFFFFFu ? wp : nP;
+      g_E = nE == 0xFFFFFFFFu ? wp : nE;
+    }
+    head = 0;
+    tail = wp;
+    __syncwarp();
+  }
+
+  // S5 for the segment engine
+  __device__ void seg_execute(uint32_t n_evict, int64_t peak, uint32_t waiting) {
+    const int L = P.n_seg;
+    const bool act = lane < L && lane <= kstar;
+    const uint32_t b = lane < L ? P.seg_b[lane] : 0u, W = lane < L ? P.seg_w[lane] : 0u;
+    uint32_t nd = 0, kvf = 0, dtok = 0, tok = 0;
+    if (act) {
+      // non-entry members run stage b_k + C_k - x: sum (l + s) = T_k + n (b_k + C_k)
+      tok = (uint32_t)(g_T + (int64_t)g_nne * (int64_t)(b + g_C));
+      if (W > 0) {  // members whose stage l' runs now complete (A8)
+        const uint32_t i = P.hoff[lane] + g_R;
+        const uint32_t c = hcnt[i], sl = hsll[i];
+        nd = c;
+        kvf = sl - c;
+        dtok = hslp[i];
+        hcnt[i] = 0; hsll[i] = 0; hslp[i] = 0;
+        g_T -= (int64_t)sl - (int64_t)c * (int64_t)(b + g_C);
+        g_nne -= c;
+      }
+    }
+    // entry stage of every active segment k >= 2: the oldest min{n_k, Q}
+    // alive residents join cohort x = C_k
+    for (uint32_t tm = __ballot_sync(FULL, act && lane >= 1 && g_nen > 0); tm; tm &= tm - 1) {
+      const int k = __ffs(tm) - 1;
+      const uint32_t need0 = min(bcast32(g_nen, k), P.thr[k]);
+      const uint32_t C = bcast32(g_C, k), R = bcast32(g_R, k), Rc = bcast32(g_Rc, k);
+      const uint32_t bk = P.seg_b[k], Wk = P.seg_w[k], ek = bk + Wk, ho = P.hoff[k];
+      const uint32_t end = bcast32(g_P, k - 1);  // entry range [E_k, P_{k-1})
+      uint32_t pos = bcast32(g_E, k), need = need0, nrec = 0;
+      uint32_t my_nne = 0, my_nx = 0, my_slx = 0;
+      int64_t my_dT = 0;
+      while (need > 0 && pos < end) {
+        const uint32_t p = pos + (uint32_t)lane;
+        const bool v = p < end;
+        SRec r = {0, 0};
+        if (v) r = sa[p];
+        const uint32_t l = r.llp & 0xFFFFu, lp = r.llp >> 16;
+        const bool alive = v && lp >= bk;
+        const uint32_t am = __ballot_sync(FULL, alive);
+        const uint32_t rk = __popc(am & lanemask_lt());
+        const bool tk = alive && rk < need;
+        const uint32_t last = __ballot_sync(FULL, alive && rk == need - 1);
+        const uint32_t ext = last ? (uint32_t)__ffs(last) : min(32u, end - pos);
+        if ((uint32_t)lane < ext) sa[p].xf = (r.xf & SX_FT) | C;
+        if (tk) {
+          tok += l + bk;
+          if (lp == bk) {  // completes at the entry stage
+            ++nd;
+            kvf += l + lp - 1;
+            dtok += lp;
+          } else {
+            ++my_nne;
+            my_dT += (int64_t)l - (int64_t)C;
+            if (lp <= ek) {
+              const uint32_t i = ho + wrapc(R + (lp - bk), Wk);
+              sh_add_u32(&hcnt[i], 1u);
+              sh_add_u32(&hsll[i], l + lp);
+              sh_add_u32(&hslp[i], lp);
+            } else {
+              ++my_nx;
+              my_slx += l;
+            }
+          }
+        }
+        nrec += ext;
+        pos += ext;
+        need -= min((uint32_t)__popc(am), need);
+      }
+      const uint32_t s_nne = __reduce_add_sync(FULL, my_nne), s_nx = __reduce_add_sync(FULL, my_nx);
+      const uint32_t s_slx = __reduce_add_sync(FULL, my_slx);
+      const int64_t s_dT = warp_sum_i64(my_dT);
+      __syncwarp();
+      if (lane == k) { g_E = pos; g_nen -= need0 - need; g_nne += s_nne; g_T += s_dT; }
+      if (lane == 0) {
+        const uint32_t ci = P.coff[k] + Rc;
+        con[ci] += nrec | (s_nx << 16);
+        col[ci] += s_slx;
+      }
+      __syncwarp();
+    }
+    // a batch ending after T is the last one; its completions are not
+    // counted (A19): their arrival ticks leave the completion sum here
+    {
+      const int64_t tokens = (int64_t)__reduce_add_sync(FULL, tok) + sum_new_l;
+      const int64_t tau = P.d0_t + P.d1_t * max(tokens - P.b0, (int64_t)0);
+      if (now + tau > P.T_t) seg_late_sum();
+    }
+    // cohort x = C_k - W_k ran stage e_k: its alive members move to the
+    // entry stage of segment k+1 (the range start moves past the cohort)
+    uint32_t ex_alive = 0;
+    if (act) {
+      const uint32_t ci = P.coff[lane] + (g_Rc == W ? 0u : g_Rc + 1);
+      const uint32_t cn = con[ci], sl = col[ci];
+      con[ci] = 0;
+      col[ci] = 0;
+      const uint32_t nx = cn >> 16;
+      g_P += cn & 0xFFFFu;
+      g_nne -= nx;
+      g_T -= (int64_t)sl - (int64_t)nx * (int64_t)(g_C - W);
+      ex_alive = nx;
+    }
+    {
+      const uint32_t from = __shfl_up_sync(FULL, ex_alive, 1);
+      if (lane >= 1 && lane < L) g_nen += from;
+    }
+    head = bcast32(g_P, L - 1);
+    // first tokens of the prompts admitted at the previous batch (stage 1)
+    const uint32_t nf = pf_n;
+    const uint64_t fta = pf_a;
+    pf_n = 0;
+    pf_a = 0;
+    // admissions (their stage-0 iteration is this batch) join cohort x = C_1 at the tail
+    if (n_new > 0) {
+      if (tail + n_new > P.seg_cap) {
+        seg_compact();
+        // a nearly full array would compact at every batch: overflow instead
+        // (status 1: the replication re-runs on the member engine)
+        if (tail + n_new + (P.seg_cap >> 3) > P.seg_cap) { status = 1; return; }
+      }
+      const uint32_t C0 = bcast32(g_C, 0), R0 = bcast32(g_R, 0), Rc0 = bcast32(g_Rc, 0), W0 = P.seg_w[0];
+      uint32_t my_nx = 0, my_slx = 0, my_pf = 0, my_l = 0;
+      uint64_t my_pfa = 0;
+      for (uint32_t j0 = 0; j0 < n_new; j0 += 32) {
+        const uint32_t j = j0 + (uint32_t)lane;
+        if (j < n_new) {
+          const Rec e = rr[j];
+          const uint32_t l = (uint32_t)(e.q & 0xFFFF), lp = (uint32_t)((e.q >> 16) & 0xFFFF);
+          const bool ft = ((uint32_t)(e.q >> 48) & META_FT) != 0;
+          sa[tail + j] = SRec{l | (lp << 16), C0 | (ft ? SX_FT : 0u)};
+          ga[tail + j] = e.a;
+          acc_adm += (uint64_t)e.a;
+          my_l += l;
+          if (!ft) { ++my_pf; my_pfa += (uint64_t)e.a; }
+          if (lp <= W0) {
+            const uint32_t i = P.hoff[0] + wrapc(R0 + lp, W0);
+            sh_add_u32(&hcnt[i], 1u);
+            sh_add_u32(&hsll[i], l + lp);
+            sh_add_u32(&hslp[i], lp);
+          } else {
+            ++my_nx;
+            my_slx += l;
+          }
+        }
+      }
+      pf_n = __reduce_add_sync(FULL, my_pf);
+      pf_a = warp_sum_u64(my_pfa);
+      const uint32_t s_nx = __reduce_add_sync(FULL, my_nx), s_slx = __reduce_add_sync(FULL, my_slx);
+      const uint32_t s_l = __reduce_add_sync(FULL, my_l);
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t ci = P.coff[0] + Rc0;
+        con[ci] += n_new | (s_nx << 16);
+        col[ci] += s_slx;
+        g_nne += n_new;
+        g_T += (int64_t)s_l - (int64_t)n_new * (int64_t)C0;
+      }
+      tail += n_new;
+      __syncwarp();
+    }
+    if (act) {
+      ++g_C;
+      if (W > 0) g_R = g_R + 1 == W ? 0u : g_R + 1;
+      g_Rc = g_Rc == W ? 0u : g_Rc + 1;
+    }
+    const uint32_t tok_o = __reduce_add_sync(FULL, tok), nd_o = __reduce_add_sync(FULL, nd);
+    const uint32_t kvf_o = __reduce_add_sync(FULL, kvf), dtok_o = __reduce_add_sync(FULL, dtok);
+    const uint32_t gr = n_plan_res - nd_o;
+    n_res = n_res - nd_o + n_new;
+    epilogue(n_evict, peak, waiting, tok_o, nd_o, nf, dtok_o, kvf_o, gr, 0ull, lane == 0 ? fta : 0ull);
+  }
+
+  // arrival-tick sum of the members completing in this batch (after the
+  // entry-stage takes): non-entry records of active segments whose
+  // completion clock x + l' - b_k is C_k; added to the evicted sum, which
+  // is subtracted from the admitted one at the end
+  __device__ void seg_late_sum() {
+    u128 al = 0;
+    for (uint32_t p0 = head; p0 < tail; p0 += 32) {
+      const uint32_t p = p0 + (uint32_t)lane;
+      const bool v = p < tail;
+      SRec r = {0, 0};
+      if (v) r = sa[p];
+      bool en;
+      const int k = seg_of(v ? p : p0, en);
+      const uint32_t kk = (uint32_t)k & 31u;
+      const uint32_t lp = r.llp >> 16, x = r.xf & SX_X;
+      const uint32_t Ck = __shfl_sync(FULL, g_C, kk);
+      if (v && !en && k <= kstar && x + lp - P.seg_b[kk] == Ck) al += (uint64_t)ga[p];
+    }
+    al = warp_sum_u128(al);
+    if (lane == 0) st->acc_ev += al;
+    __syncwarp();
+  }
+
+  // end of a replication: arrival-tick sum of the residents still alive, so
+  // that sum over completions by T of a = admitted - evicted - late - alive
+  __device__ void seg_finish() {
+    u128 ares = 0;
+    for (uint32_t p0 = head; p0 < tail; p0 += 32) {
+      const uint32_t p = p0 + (uint32_t)lane;
+      const bool v = p < tail;
+      SRec r = {0, 0};
+      int64_t a = 0;
+      if (v) { r = sa[p]; a = ga[p]; }
+      bool en;
+      const int k = seg_of(v ? p : p0, en);
+      const uint32_t kk = (uint32_t)k & 31u;
+      const uint32_t lp = r.llp >> 16, x = r.xf & SX_X;
+      const uint32_t Ck = __shfl_sync(FULL, g_C, kk);
+      const uint32_t bk = P.seg_b[kk];
+      const bool alive = en ? lp >= bk : bk + Ck - x <= lp;
+      if (v && alive) ares += (uint64_t)a;
+    }
+    ares = warp_sum_u128(ares);
+    if (lane == 0) st->acc_done_a = st->acc_adm - st->acc_ev - ares;
+    __syncwarp();
+  }
+
   // per-lane batch accumulators of the execute pass
   struct Acc {
     uint32_t tok = 0, n_done = 0, done_tok = 0, n_ft = 0, kv_free = 0, grow = 0;
@@ -1426,6 +1899,7 @@ struct WarpSim {
   // One pass over residents (+ the staged admissions) in admission order:
   // per-member update, completions, compaction; counters updated in place.
   __device__ void execute(uint32_t n_evict, int64_t peak, uint32_t waiting) {
+    if (SEG) { seg_execute(n_evict, peak, waiting); return; }
     uint32_t tok, nd, nf, dtok, kvf, gr;
     uint64_t done_a = 0, ft_a = 0;
     if (RING) {
@@ -1676,12 +2150,21 @@ struct WarpSim {
     }
     __syncwarp();
     k_vis = vbase = k_adm = abase = pcount = rhead = rtail = 0;
-    if (lane < P.n_rings) rq[4 * lane] = rq[4 * lane + 2] = kNoChunk;
+    if (lane < P.n_rings) rq[8 * lane] = rq[8 * lane + 2] = kNoChunk;
     vprev = aprev = 0;
     newc = 0;
     r_head = r_n = r_C = seq_next = 0;
     r_X = 0;
     if (RING) psum()[lane] = 0;
+    if (SEG) {
+      head = tail = 0;
+      pf_n = 0; pf_a = 0;
+      acc_adm = acc_ev = 0;
+      g_P = g_E = g_C = g_R = g_Rc = g_nne = g_nen = 0;
+      g_T = 0;
+      for (uint32_t i = lane; i < P.hsize; i += 32) { hcnt[i] = 0; hsll[i] = 0; hslp[i] = 0; }
+      for (uint32_t i = lane; i < P.csize; i += 32) { con[i] = 0; col[i] = 0; }
+    }
     for (int c = 0; c < P.K; ++c) {
       fill<true>(c, 0, 0, vt, vl, vlp);
     }
@@ -1698,6 +2181,7 @@ struct WarpSim {
       int64_t peak = 0;
       if (go) {
         if (RING) memory_ring(n_evict, peak);
+        else if (SEG) seg_memory(n_evict, peak);
         else memory(n_evict, peak);
         if (status) break;
         if (n_plan_res + n_new == 0) go = false;    // empty after eviction: wait (R27)
@@ -1713,7 +2197,7 @@ struct WarpSim {
       // admissions are final: return the restart chunks the heads passed
       if (lane < P.n_rings) fifo_commit(lane, rhead);
       execute(n_evict, peak, waiting);
-      if (RING && status) break;
+      if ((RING || SEG) && status) break;
     }
     finish();
   }
@@ -1723,6 +2207,7 @@ struct WarpSim {
     if (lane < P.n_rings) fifo_release_all(lane);
     flush_acc();
     __syncwarp();
+    if (SEG) seg_finish();
     const WarpStats S = *st;
     const uint64_t arrivals = S.arrivals, completed = S.completed;
     const u128 lat = S.sum_done_t - S.acc_done_a;
@@ -1764,7 +2249,7 @@ struct WarpSim {
   }
 };
 
-template <int POL, bool TRACE, bool RING>
+template <int POL, bool TRACE, bool RING, bool SEG>
 // WAIT: <= 4 warps per block, 5 blocks per SM -> <= 102 registers (20 warps/SM
 // at C2's shared-memory footprint); others are shared-memory bound: 128 regs
 __global__ void __launch_bounds__(POL == SCHED_WAIT ? 128 : 256, POL == SCHED_WAIT ? 5 : 2)
@@ -1772,7 +2257,8 @@ __global__ void __launch_bounds__(POL == SCHED_WAIT ? 128 : 256, POL == SCHED_WA
   extern __shared__ __align__(16) unsigned char smem[];
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  WarpSim<POL, TRACE, RING> sim(P, smem + (size_t)wib * P.warp_smem, lane);
+  const uint32_t slot = blockIdx.x * (blockDim.x >> 5) + (uint32_t)wib;  // SEG: global per-warp array
+  WarpSim<POL, TRACE, RING, SEG> sim(P, smem + (size_t)wib * P.warp_smem, lane, slot);
   for (;;) {
     uint32_t i = 0;
     if (lane == 0) i = atomicAdd(P.work_counter, 1u);
@@ -1788,20 +2274,21 @@ __global__ void __launch_bounds__(POL == SCHED_WAIT ? 128 : 256, POL == SCHED_WA
     if (!P.fallback && P.retry_list && sim.status == 1 && lane == 0)
       P.retry_list[atomicAdd(P.retry_count, 1u)] = r;  // re-run with the safe capacity
   }
+  sim.flush_stash();
 }
 
-template <int POL, bool TRACE, bool RING = false>
+template <int POL, bool TRACE, bool RING = false, bool SEG = false>
 cudaError_t launch_t(const DevParams& p, int grid, int block, size_t smem, cudaStream_t s) {
-  auto k = sim_kernel<POL, TRACE, RING>;
+  auto k = sim_kernel<POL, TRACE, RING, SEG>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<grid, block, smem, s>>>(p);
   return cudaGetLastError();
 }
 
-template <int POL, bool TRACE, bool RING = false>
+template <int POL, bool TRACE, bool RING = false, bool SEG = false>
 cudaError_t occ_t(int block, size_t smem, int* bps) {
-  auto k = sim_kernel<POL, TRACE, RING>;
+  auto k = sim_kernel<POL, TRACE, RING, SEG>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k, block, smem);
@@ -1811,6 +2298,10 @@ cudaError_t occ_t(int block, size_t smem, int* bps) {
 }  // namespace
 
 cudaError_t launch_sim(const DevParams& p, int grid, int block, size_t smem, cudaStream_t s) {
+  if (p.seg_engine) {
+    if (p.trace_mode) return launch_t<SCHED_NESTED, true, false, true>(p, grid, block, smem, s);
+    return launch_t<SCHED_NESTED, false, false, true>(p, grid, block, smem, s);
+  }
   if (p.trace_mode) {
     switch (p.policy) {
       case SCHED_WAIT: return launch_t<SCHED_WAIT, true>(p, grid, block, smem, s);
@@ -1835,6 +2326,10 @@ cudaError_t launch_sim(const DevParams& p, int grid, int block, size_t smem, cud
 }
 
 cudaError_t sim_occupancy(int policy, int trace, int block, size_t smem, int* bps, int ring) {
+  if (ring == 2) {
+    if (trace) return occ_t<SCHED_NESTED, true, false, true>(block, smem, bps);
+    return occ_t<SCHED_NESTED, false, false, true>(block, smem, bps);
+  }
   if (ring) {
     switch (policy) {
       case SCHED_WAIT: return occ_t<SCHED_WAIT, false, true>(block, smem, bps);

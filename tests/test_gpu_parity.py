@@ -230,14 +230,19 @@ def test_sharding_invariance_and_determinism():
         assert np.array_equal(np.concatenate(parts, axis=1), full)
 
 
+@pytest.mark.parametrize("engine", ["member", "seg"])
 @pytest.mark.parametrize("spec", [32, 64, 256])
-def test_speculative_capacity_fallback(spec):
+def test_speculative_capacity_fallback(spec, engine, monkeypatch):
     """Replications overflowing the speculative capacity are re-run by the
-    fallback launch with the safe capacity: rows stay bit-exact."""
+    fallback launch with the safe capacity: rows stay bit-exact.  (Segment
+    engine: its array is 1.5x the member engine's speculative population plus
+    two admission batches; overflow re-runs on the member engine.)"""
     from paper_2504_11320_b200 import Scheduler
+    monkeypatch.setenv("WAITSIM_ENGINE", engine)
     s = Scheduler(W.C3A, W.Policy(W.NESTED, seg_end=SEG3A), [7, 7, 7, 5], spec_resident=spec)
     li = s.launch_info()
-    assert li["spec_resident"] == spec and li["fallback_grid"] > 0
+    want = spec if engine == "member" else ((int(1.5 * spec) + 14 + 31) // 32) * 32
+    assert li["spec_resident"] == want and li["fallback_grid"] > 0
     got = s.run_host(W.C3A.seed, 0, 24, 20.0)
     ref = oracle.run(W.C3A, W.Policy(W.NESTED, seg_end=SEG3A), [7, 7, 7, 5], n_reps=24, n_threads=8,
                      horizon_s=20.0)
@@ -386,13 +391,16 @@ def test_idle_skip_partial_jumps():
 def test_engine_selection_rule(monkeypatch):
     """class-ring engine for fixed-length WAIT / short-decode
     FCFS unless its footprint exceeds the member engine's by > 30%; Nested
-    and marks always use the member engine."""
+    uses the segment engine; marks under WAIT / FCFS the member engine."""
     from paper_2504_11320_b200 import Scheduler
     monkeypatch.delenv("WAITSIM_ENGINE", raising=False)
     eng = lambda wl, pol, thr=None: Scheduler(wl, pol, thr).launch_info()["engine"]
     assert eng(W.C2, W.Policy(W.WAIT), [16, 16]) == 1
     assert eng(W.C2, W.Policy(W.FCFS, B=1024)) == 1
+    assert eng(W.C3A, W.Policy(W.NESTED, seg_end=SEG3A), [7, 7, 7, 5]) == 2
+    monkeypatch.setenv("WAITSIM_ENGINE", "member")
     assert eng(W.C3A, W.Policy(W.NESTED, seg_end=SEG3A), [7, 7, 7, 5]) == 0
+    monkeypatch.delenv("WAITSIM_ENGINE")
     assert eng(W.C3B, W.Policy(W.FCFS, B=2048)) == 0                 # marks
     assert eng(W.c4(1), W.Policy(W.FCFS, B=1024)) == 0               # long decodes
     assert eng(W.c4(4), W.Policy(W.WAIT), [18, 12, 6]) == 0          # rings 6,036 records vs 4,096
@@ -481,11 +489,12 @@ def test_hand_traces_replayed(case):
 # ------------------------------------------------ restart pool
 def test_restart_pool_chunks_are_reused():
     """C1 WAIT evicts ~280 prompts per replication; 16,384 replications push
-    ~4.6M restart entries through a pool of 2^18 (4,096 chunks): chunks are
+    ~4.6M restart entries through a pool of 2^19 (8,192 chunks, more than
+    the ~4,700 warps in flight each hold while a restart waits): chunks are
     returned and reused, every row has status 0, sampled rows equal the
     oracle and the high-water mark stays within the pool."""
     from paper_2504_11320_b200 import Scheduler
-    s = Scheduler(W.C1, W.Policy(W.WAIT), [1], restart_cap=1 << 18)
+    s = Scheduler(W.C1, W.Policy(W.WAIT), [1], restart_cap=1 << 19)
     rows = s.run_host(W.C1.seed, 0, 16384, W.C1.horizon_s)
     pool = s.restart_pool()
     s.close()
@@ -510,3 +519,60 @@ def test_restart_pool_exhaustion_is_reported():
     for i in ok:
         ref = oracle.run(W.C1, W.Policy(W.WAIT), [1], n_reps=1, rep_begin=i)
         assert_rows_equal(rows[:, i:i + 1], ref, f"C1 rep {i}")
+
+
+# ------------------------------- Nested: segment engine vs member engine
+@pytest.mark.parametrize("engine", ["member", "seg"])
+@pytest.mark.parametrize("case", ["c1", "c3a", "c3b", "c4_evict", "c5_thrash", "k12", "random", "tight_cap",
+                                  "one_stage_segments"])
+def test_nested_engines_bit_exact(engine, case, monkeypatch):
+    """The member engine and the segment engine (residents in
+    admission order = stage order, completion histograms per segment,
+    cohorts leaving as blocks, tombstones and compaction) are two layouts of
+    Algorithm 2's semantics: forced either way, every
+    row matches the oracle -- LIFO eviction into entry-stage queues, late
+    last batches, completions at entry stages (one-stage segments) and
+    compaction under a tight array (tight_cap) included."""
+    from paper_2504_11320_b200 import Scheduler
+    monkeypatch.setenv("WAITSIM_ENGINE", engine)
+    kw, T = {}, None
+    if case == "c1":
+        wl, seg, thr, n = W.C1, [16], [1], 64
+    elif case == "c3a":
+        wl, seg, thr, n, T = W.C3A, SEG3A, W.PAPER_NESTED_RATIO_C3A, 24, 20.0
+    elif case == "c3b":
+        wl, seg, n, T = W.C3B, SEG10, 16, 20.0
+        thr = fl.nested_strict(wl, seg)
+    elif case == "c4_evict":
+        wl, seg, n, T = W.c4(3), SEG4, 12, 8.0
+        thr = fl.nested_strict(wl, seg)
+    elif case == "c5_thrash":
+        wl, seg, n, T = W.c5(55.0), SEG10, 8, 200.0
+        thr = fl.nested_strict(wl, seg)
+    elif case == "k12":
+        wl = W.Workload("k12", [10.0, 40, 0, 90] * 3, [W.fixed(2)] * 12, [[(1, 5), (3, 2), (9, 1)]] * 12,
+                        M=120, horizon_s=1.0, seed=77, d0_s=0.004, d1_s=2e-4)
+        seg, thr, n = [2, 5, 9], [4, 3, 2], 16
+    elif case == "random":
+        rng = np.random.default_rng(7)
+        for _ in range(8):
+            wl = W.random_small(rng, horizon_s=1.5)
+            maxlp = max(v for t in wl.lp_tab for v, _ in t)
+            seg = sorted({int(x) for x in rng.integers(1, maxlp + 1, 3)} | {maxlp})
+            thr = sorted([int(x) for x in rng.integers(1, 6, len(seg))], reverse=True)
+            check(wl, W.Policy(W.NESTED, seg_end=seg), thr, 16)
+        return
+    elif case == "tight_cap":
+        monkeypatch.setenv("WAITSIM_SEG_CAP", "0.5")
+        wl, seg, thr, n, T = W.C3A, SEG3A, [7, 7, 7, 5], 32, 6.0
+    else:  # segments of one stage: entry stage = last stage (W_k = 0)
+        wl = W.Workload("w0", [30.0, 20.0], [W.fixed(3), [(1, 2), (6, 1)]], [[(2, 1), (3, 1), (4, 2)], W.fixed(5)],
+                        M=90, horizon_s=3.0, seed=123, d0_s=0.01, d1_s=1e-4)
+        seg, thr, n = [2, 3, 4, 5], [3, 3, 2, 2], 24
+    got = check(wl, W.Policy(W.NESTED, seg_end=seg), thr, n, horizon_s=T, **kw)
+    s = Scheduler(wl, W.Policy(W.NESTED, seg_end=seg), thr)
+    assert s.launch_info()["engine"] == (2 if engine == "seg" else 0)
+    s.close()
+    f = lambda k: got[oracle.F[k]].astype(object)
+    assert (f("arrivals") == f("completed") + f("completed_after_T") + f("final_waiting")
+            + f("final_resident")).all()
