@@ -89,6 +89,13 @@ struct sched_s {
   bool use_ring = false;                     // sched_run uses the class-ring engine
   bool use_seg = false;                      // sched_run / sched_run_trace use the segment engine
   int64_t* d_seg_a = nullptr;                // segment engine: per-warp arrival-tick arrays
+  void* d_ring_g = nullptr;                  // class-ring engine: per-warp ring records (16 B)
+  uint64_t ring_g_cap = 0;
+  uint8_t* d_ring_log = nullptr;             // class-ring engine: per-warp admission logs (2^16 B)
+  uint32_t* d_pool_stash = nullptr;          // per-slot restart-chunk stashes
+  uint64_t stash_words = 0;
+  uint64_t ring_log_warps = 0;
+  uint32_t ring_stride = 0;
   size_t seg_a_cap = 0;
   double n_star_c[32] = {};                  // fluid prompts in service per class
   double m_star = 0;                         // fluid KV occupancy M*
@@ -263,12 +270,21 @@ int prepare(sched_s* h) {
     h->base.hsize = ho;
     h->base.csize = co;
   }
+  // class-ring engine: cohort-count rings, l'_c + 1 slots per class
+  if (h->in.policy != SCHED_NESTED) {
+    uint32_t co = 0;
+    for (int c = 0; c < (int)h->in.lambda.size() && c < 32; ++c) {
+      h->base.ccoff[c] = co;
+      co += (uint32_t)h->in.lp[c].back().first + 1u;
+    }
+    h->base.ccsize = co;
+  }
   // choose warps per block maximising resident warps per SM
   auto size_launch = [&](bool ring, uint32_t records, uint32_t* wsm, int* wpb_out, int* bps_out,
                          uint32_t seg_cap = 0) -> int {
     *wsm = warp_smem_bytes(records, K, h->tv_any, ring, h->in.policy == SCHED_NESTED,
                            h->in.policy == SCHED_WAIT ? (uint32_t)K : 1u, seg_cap, h->base.hsize,
-                           h->base.csize);
+                           h->base.csize, ring ? h->base.ccsize * 4u : 0u);
     int best_w = 0;
     const int cands[] = {8, 4, 2, 1};
     for (int wpb : cands) {
@@ -289,9 +305,8 @@ int prepare(sched_s* h) {
   auto size_cfg = [&](LaunchCfg& L) -> int {
     uint32_t rec = L.Rc, rec_safe = L.Rc_safe;
     if (L.ring) {
-      rec += L.spare;  // spare staging slots: eviction-round victims
+      rec += L.spare;  // spare staging slots: eviction-round victims (the rings are in global memory)
       rec_safe += L.spare;
-      for (int c = 0; c < K; ++c) { rec += L.rcap[c]; rec_safe += L.rcap_safe[c]; }
     }
     L.fallback = rec < rec_safe;
     int wpb = 1, bps = 0;
@@ -367,17 +382,7 @@ int prepare(sched_s* h) {
       // admissions per batch ~ Poisson(adm): mean + 8 sd + 16 (tail < 1e-12)
       L.Rc = std::min<uint32_t>(L.Rc_safe, round32((uint64_t)(adm + 8.0 * std::sqrt(adm)) + 16));
     }
-    // victim slots per eviction round: 32 when memory binds (WAIT: M^pi > M,
-    // FCFS: M* > M), else 8 (evictions rare: save the shared memory)
-    {
-      double mpi = 0;
-      for (int c = 0; c < K && in.policy == SCHED_WAIT; ++c) {
-        const double l = in.l[c][0].first, lp = in.lp[c][0].first;
-        mpi += in.thresholds[c] * (lp * l + lp * (lp + 1) / 2);
-      }
-      const bool binds = in.policy == SCHED_WAIT ? mpi > (double)in.M : h->m_star > (double)in.M;
-      L.spare = binds ? 32u : 8u;
-    }
+    L.spare = 0;  // LIFO victims are read in place (admission log): no staging slots
     // a ring footprint that does not fit in shared memory only makes the
     // ring engine ineligible (the member engine runs), unless it was forced
     const bool forced = eng && std::string(eng) == "ring";
@@ -385,22 +390,29 @@ int prepare(sched_s* h) {
       if (forced) return rc;
       L.grid = 0;
     }
-    // the ring engine does O(classes + events) work per batch but its
-    // per-class capacities can cost occupancy: keep it unless its
-    // speculative footprint exceeds the member engine's by > 30%
-    // (measured: C2, C4 rho=0.5/0.8 WAIT and C2 FCFS gain; C4 rho=0.95 WAIT
-    // and long-l' FCFS lose)
-    uint64_t ring_rec = L.Rc + L.spare;
-    for (int c = 0; c < K; ++c) ring_rec += L.rcap[c];
-    // FCFS additionally only for short decodes: with l' >> 1 most of an FCFS
-    // batch is the fixed per-batch control both engines share and the ring
-    // engine's lower occupancy loses (measured: C2 l' <= 20 +13%, C4 l' >=
-    // 100 -5..-12%)
-    double lam = 0, lam_lp = 0;
-    for (int c = 0; c < K; ++c) { lam += in.lambda[c]; lam_lp += in.lambda[c] * in.lp[c][0].first; }
-    const bool short_lp = lam > 0 && lam_lp / lam <= 64.0;
-    h->use_ring = L.grid > 0 && (forced || ((double)ring_rec <= 1.3 * (double)h->mem.Rc &&
-                                            (in.policy == SCHED_WAIT || short_lp)));
+    // the ring engine does O(classes + admissions) work per batch and keeps
+    // only staging slots and per-clock cohort counts in shared memory (the
+    // member records live in global memory, read by evictions and at the
+    // end of a replication): every eligible configuration uses it
+    h->use_ring = L.grid > 0;
+    if (h->use_ring) {
+      uint64_t stride = 0;
+      for (int c = 0; c < K; ++c) stride += L.rcap_safe[c];
+      const uint64_t warps = std::max<uint64_t>((uint64_t)L.grid * L.wpb, (uint64_t)L.fb_grid * L.fb_wpb);
+      h->ring_stride = (uint32_t)stride;
+      if (warps * stride > h->ring_g_cap) {
+        cudaFree(h->d_ring_g);
+        h->d_ring_g = nullptr;
+        CK(cudaMalloc(&h->d_ring_g, warps * stride * 16));
+        h->ring_g_cap = warps * stride;
+      }
+      if (warps > h->ring_log_warps) {
+        cudaFree(h->d_ring_log);
+        h->d_ring_log = nullptr;
+        CK(cudaMalloc(&h->d_ring_log, warps << 16));
+        h->ring_log_warps = warps;
+      }
+    }
   }
   // segment engine (NESTED): O(entry-stage takes + admissions) per batch
   // instead of a pass over every resident; replications
@@ -467,6 +479,27 @@ int prepare(sched_s* h) {
   p.pool_bump = (uint32_t*)(h->d_pool_free + 1);
   p.pool_chunks = h->pool_chunks;
   p.work_counter = h->d_counter;
+  {
+    // per-slot restart-chunk stashes: slots of the widest launch of any engine
+    uint64_t slots = 1;
+    for (const LaunchCfg* L : {&h->mem, &h->rng, &h->sg}) {
+      slots = std::max<uint64_t>(slots, (uint64_t)L->grid * L->wpb);
+      slots = std::max<uint64_t>(slots, (uint64_t)L->fb_grid * L->fb_wpb);
+    }
+    const uint64_t words = slots * (uint64_t)n_rings * 12;
+    if (words > h->stash_words) {
+      // chunks held by an old stash array are not returned (bounded: 11 per slot and ring)
+      cudaFree(h->d_pool_stash);
+      h->d_pool_stash = nullptr;
+      CK(cudaMalloc(&h->d_pool_stash, words * 4));
+      CK(cudaMemset(h->d_pool_stash, 0, words * 4));
+      h->stash_words = words;
+    }
+    p.pool_stash = h->d_pool_stash;
+  }
+  p.ring_g = h->d_ring_g;
+  p.ring_log = h->d_ring_log;
+  p.ring_stride = h->ring_stride;
   h->prepared = true;
   return 0;
 }
@@ -480,7 +513,7 @@ void set_caps(DevParams& p, const LaunchCfg& L, bool safe, int K) {
   p.warp_smem = safe ? L.fb_warp_smem : L.warp_smem;
   uint32_t off = 0;
   for (int c = 0; c < K; ++c) {
-    p.rcap[c] = L.ring ? (safe ? L.rcap_safe[c] : L.rcap[c]) : 0u;
+    p.rcap[c] = L.ring ? L.rcap_safe[c] : 0u;
     p.roff[c] = off;
     off += p.rcap[c];
   }
@@ -890,7 +923,7 @@ int sched_get_launch_info(sched_t h, sched_launch_info* out) {
   // capacities in resident records (ring engine: rings + staging slots)
   const LaunchCfg& L = h->use_seg ? h->sg : h->use_ring ? h->rng : h->mem;
   uint32_t spec = L.seg ? L.seg_cap : L.Rc, safe = L.seg ? h->mem.Rc_safe : L.Rc_safe;
-  for (int c = 0; L.ring && c < (int)h->in.lambda.size(); ++c) { spec += L.rcap[c]; safe += L.rcap_safe[c]; }
+  for (int c = 0; L.ring && c < (int)h->in.lambda.size(); ++c) { spec += L.rcap_safe[c]; safe += L.rcap_safe[c]; }
   out->grid = L.grid;
   out->block = L.block;
   out->warps_per_block = L.wpb;
@@ -974,6 +1007,9 @@ void sched_destroy(sched_t h) {
   cudaFree(h->d_stage_info);
   cudaFree(h->d_pool_a);
   cudaFree(h->d_seg_a);
+  cudaFree(h->d_ring_g);
+  cudaFree(h->d_ring_log);
+  cudaFree(h->d_pool_stash);
   cudaFree(h->d_pool_e);
   cudaFree(h->d_pool_llp);
   cudaFree(h->d_pool_next);

@@ -37,7 +37,12 @@ struct DevParams {
   uint32_t ring_engine;
   uint32_t spare;                  // staging slots beyond Rc for eviction-round victims (8 or 32)
   uint32_t rcap[kMaxClasses];      // ring capacity (records) of class c
-  uint32_t roff[kMaxClasses];      // first record of ring c after the staging area
+  uint32_t roff[kMaxClasses];      // first record of ring c in this warp's slot of ring_g
+  uint8_t* ring_log;               // [warps of the launch][2^16] class of each admission, in order
+  void* ring_g;                    // [warps of the launch][ring_stride] ring records (global: read
+  uint32_t ring_stride;            //   only by evictions and at the end of a replication)
+  uint32_t ccoff[kMaxClasses];     // cohort-count ring of class c (l'_c + 1 slots, shared memory)
+  uint32_t ccsize;
   uint32_t fl[kMaxClasses];        // fixed l | l' << 16 of class c
   // segment engine (NESTED): residents in one admission-
   // ordered array that is sorted by stage, segment k a contiguous range;
@@ -83,6 +88,7 @@ struct DevParams {
   unsigned long long* pool_free;  // free-stack head
   uint32_t* pool_bump;     // chunks handed out so far (high-water mark)
   uint32_t pool_chunks;
+  uint32_t* pool_stash;    // [warp slots][n_rings] x {count, 11 chunks}: per-slot free chunks (persist)
   uint32_t* work_counter;  // this launch's replication counter
   // speculative capacity: the main launch runs with a small resident
   // capacity; replications that overflow it are appended to retry_list and
@@ -100,8 +106,9 @@ struct DevParams {
 // shared-memory bytes per warp for a given resident capacity / class count
 inline uint32_t warp_smem_bytes(uint32_t Rc, int K, bool tv = false, bool ring = false, bool nested = false,
                                 uint32_t n_rings = 1, uint32_t seg_cap = 0, uint32_t hsize = 0,
-                                uint32_t csize = 0) {
+                                uint32_t csize = 0, uint32_t extra = 0) {
   uint32_t b = Rc * 16u;                    // residents: a (i64) + packed (l, l', s, meta)
+  b += (extra + 15u) & ~15u;                // class-ring engine: cohort counts per class clock slot
   // segment engine: staging (Rc) + resident array (8 B records; arrival
   // ticks in global memory) + histograms (3 x u32 per bucket) + cohort rings
   // (2 x u32 per slot) + eviction scratch
@@ -115,7 +122,7 @@ inline uint32_t warp_smem_bytes(uint32_t Rc, int K, bool tv = false, bool ring =
   if (nested) b += ((Rc + 31u) / 32u + 15u) & ~15u;  // per-chunk activity summaries
   if (tv) b += (uint32_t)K * (32u * 16u);   // operational-time windows (generated, private)
   b = (b + 15u) & ~15u;
-  b += n_rings * 32u;                        // restart FIFO chunk cursors (head, head index, tail, tail index) + chunk stash
+  b += n_rings * 64u;                        // restart FIFO chunk cursors (head, head index, tail, tail index) + chunk stash
   return b;
 }
 

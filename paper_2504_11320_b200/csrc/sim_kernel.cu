@@ -178,6 +178,7 @@ struct __align__(16) RRec {
   uint32_t seq;
 };
 constexpr uint32_t XF_FT = 0x80000000u, XF_PEND = 0x40000000u, XF_X = 0x3FFFFFFFu;
+constexpr uint32_t kRingLog = 1u << 16;  // admission-log entries per warp (class-ring engine)
 // segment-engine resident (NESTED), shared memory: l | l' << 16,
 // cohort clock x (bits 0-30: the segment clock at which it ran its entry
 // stage; stage = b_k + C_k - x) | first token emitted before a restart (bit
@@ -201,6 +202,10 @@ __device__ __forceinline__ uint32_t count_before(const int64_t* v, uint32_t n, i
   return lo;
 }
 
+struct WarpStats;
+__device__ __noinline__ void flush_sums(WarpStats* st, int lane, uint64_t a0, uint64_t a1, uint64_t a2,
+                                       uint64_t a3, uint64_t a4);
+
 // per-replication metric accumulators, one per warp in shared memory
 // (updated once per batch by lane 0; keeps them out of the register file)
 struct __align__(16) WarpStats {
@@ -212,6 +217,19 @@ struct __align__(16) WarpStats {
   u128 acc_adm, acc_ev;                 // segment engine: admitted / evicted arrival-tick sums
 };
 static_assert(sizeof(WarpStats) <= 256, "WarpStats slot");
+
+// lane-local arrival-tick sums -> 128-bit warp totals (out of line: rarely
+// run, and keeps the per-batch instruction footprint small)
+__device__ __noinline__ void flush_sums(WarpStats* st, int lane, uint64_t a0, uint64_t a1, uint64_t a2,
+                                       uint64_t a3, uint64_t a4) {
+  const u128 s0 = warp_sum_u128(a0), s1 = warp_sum_u128(a1), s2 = warp_sum_u128(a2);
+  const u128 s3 = warp_sum_u128(a3), s4 = warp_sum_u128(a4);
+  if (lane == 0) {
+    st->acc_arr += s0; st->acc_done_a += s1; st->acc_ft_a += s2;
+    st->acc_adm += s3; st->acc_ev += s4;
+  }
+  __syncwarp();
+}
 
 // arrival tick at operational time tau of a time-varying class: invert the
 // integrated piecewise-constant rate
@@ -297,7 +315,8 @@ struct WarpSim {
   const int lane;
   // shared-memory views (this warp's slice)
   Rec* rr;                           // [Rc] residents in admission order (RING: staged admissions)
-  RRec* rg;                          // RING: class rings (ring c: P.rcap[c] records from P.roff[c])
+  RRec* rg;                          // RING: class rings in global memory (ring c: P.rcap[c] records from P.roff[c])
+  uint32_t* coh;                     // RING: [ccsize] members admitted at class clock x, slot x mod (l'_c + 1)
   int64_t* vt;                       // [K][32] generated window (t): visibility + admission
   uint16_t* vl; uint16_t* vlp;       // [K][32] generated window (l, l')
   int64_t* at;                       // [K][32] private admission windows (t)
@@ -310,7 +329,7 @@ struct WarpSim {
   WarpStats* st;                     // metric accumulators
   uint64_t* xs;                      // [32] RING eviction scratch (per-class sums)
   uint8_t* csum;                     // NESTED: per-chunk lowest resident segment
-  uint32_t* rq;                      // [n_rings][8] restart FIFO chunks: head, head index, tail, tail index, stash
+  uint32_t* rq;                      // [n_rings][16] restart FIFO chunks: head, head index, tail, tail index, stash
   // SEG (NESTED segment engine): residents in one array in
   // admission order = stage order; segment k is the range [P_k, P_{k-1})
   // (k = 0: [P_0, tail)), non-entry part [P_k, E_k), entry-stage part
@@ -336,6 +355,9 @@ struct WarpSim {
   // RING: lane c holds class c's ring (head position, residents, clock =
   // batches class c took part in, sum of admission clocks) + next sequence no.
   uint32_t r_head, r_n, r_C, seq_next;
+  uint32_t r_Ri;                     // r_C mod (l'_c + 1): cohort slot of the current clock
+  uint32_t seq_max;                  // RING: admissions ever logged (uniform; the log keeps the last kRingLog)
+  uint32_t wslot;                    // this warp's slot in the per-warp global arrays
   uint64_t r_X;
   // RING: first tokens pending at class c's next participation: count in
   // cnt[32 + c], arrival-tick sum in psum()[c] (the NESTED rank / snap slots)
@@ -349,7 +371,7 @@ struct WarpSim {
   uint32_t head, tail;               // uniform
   uint32_t pf_n;                     // uniform: first tokens due at the next batch (stage 1) ...
   uint64_t pf_a;                     // ... and their arrival-tick sum
-  uint64_t acc_adm, acc_ev;          // lane-local arrival-tick sums of admissions / evictions
+  uint64_t acc_adm, acc_ev;          // SEG / RING: lane-local arrival-tick sums of admissions / evictions
 
   // replication
   uint32_t rep, rglob;
@@ -368,9 +390,14 @@ struct WarpSim {
       : P(p), lane(lane_) {
     const uint32_t Rc = p.Rc;
     rr = (Rec*)base;
-    // RING: 32 spare staging slots hold the victims of one eviction round
-    rg = (RRec*)(rr + Rc + (RING ? p.spare : 0u));
-    vt = (int64_t*)(rr + Rc + (RING ? p.spare + p.roff[p.K - 1] + p.rcap[p.K - 1] : 0u));
+    // RING: spare staging slots hold the victims of one eviction round
+    vt = (int64_t*)(rr + Rc);
+    if (RING) {
+      rg = (RRec*)p.ring_g + (size_t)slot * p.ring_stride;
+      coh = (uint32_t*)(rr + Rc + p.spare);
+      vt = (int64_t*)((unsigned char*)coh + ((p.ccsize * 4u + 15u) & ~15u));
+    }
+    wslot = slot;
     if (SEG) {
       ga = p.seg_a + (size_t)slot * p.seg_cap;
       sa = (SRec*)(rr + Rc);
@@ -398,42 +425,46 @@ struct WarpSim {
     vtau = (int64_t*)((unsigned char*)st + ((RING || SEG) ? 512 : 256) +
                       (POL == SCHED_NESTED ? (((p.Rc + 31) / 32 + 15) & ~15u) : 0u));
     atau = vtau + p.K * 32;
-    rq = (uint32_t*)(base + p.warp_smem - p.n_rings * 32u);
-    if (lane < p.n_rings) rq[8 * lane + 4] = 0;  // empty chunk stash
+    rq = (uint32_t*)(base + p.warp_smem - p.n_rings * 64u);
+    if (lane < p.n_rings) {  // this slot's chunk stash, kept in global memory between launches
+      const uint4* g = reinterpret_cast<const uint4*>(p.pool_stash) + ((size_t)slot * p.n_rings + lane) * 3;
+      for (int i = 0; i < 3; ++i) {  // count + kStash chunks = 12 words
+        const uint4 sv = g[i];
+        rq[16 * lane + 4 + 4 * i] = sv.x; rq[16 * lane + 5 + 4 * i] = sv.y;
+        rq[16 * lane + 6 + 4 * i] = sv.z; rq[16 * lane + 7 + 4 * i] = sv.w;
+      }
+    }
   }
 
   __device__ void flush_acc() {
-    const u128 a = warp_sum_u128(acc_arr), b = warp_sum_u128(acc_done_a), c = warp_sum_u128(acc_ft_a);
-    if (lane == 0) { st->acc_arr += a; st->acc_done_a += b; st->acc_ft_a += c; }
+    flush_sums(st, lane, acc_arr, acc_done_a, acc_ft_a, (SEG || RING) ? acc_adm : 0ull,
+               (SEG || RING) ? acc_ev : 0ull);
     acc_arr = acc_done_a = acc_ft_a = 0;
-    if (SEG) {
-      const u128 d = warp_sum_u128(acc_adm), e = warp_sum_u128(acc_ev);
-      if (lane == 0) { st->acc_adm += d; st->acc_ev += e; }
-      acc_adm = acc_ev = 0;
-    }
+    if (SEG || RING) acc_adm = acc_ev = 0;
   }
   __device__ __forceinline__ void maybe_flush() {
     uint64_t m = acc_arr | acc_done_a | acc_ft_a;
-    if (SEG) m |= acc_adm | acc_ev;
+    if (SEG || RING) m |= acc_adm | acc_ev;
     if (__any_sync(FULL, (m >> 60) != 0)) flush_acc();
   }
 
   // ------------------------------------------- restart FIFOs (chunk pool)
   // FIFO q holds positions [rhead, rtail) (lane q's counters) in a linked
-  // list of kRestartChunk-entry chunks: rq[8q] = chunk of position
-  // rhead (index rq[8q+1] = its position / kRestartChunk), rq[8q+2] = chunk
-  // of the next write position rtail (index rq[8q+3]).  Chunks come from a
-  // per-FIFO stash of up to kStash free chunks (rq[8q+4] = count, rq[8q+5..]
-  // = chunks; kept across this warp's replications, returned at kernel
-  // exit), else the device-wide pool: a lock-free free stack (ABA tag in the
-  // high word), else never-used chunks.  The stash keeps the global free
-  // stack -- one hot word -- off the path of eviction-heavy runs (C5: a
-  // chunk every few batches per warp).  A chunk is returned when the
-  // committed head passes it and at the end of the replication.
-  static constexpr uint32_t kStash = 3;
+  // list of kRestartChunk-entry chunks: rq[16q] = chunk of position rhead
+  // (index rq[16q+1] = its position / kRestartChunk), rq[16q+2] = chunk of
+  // the next write position rtail (index rq[16q+3]).  Free chunks come from
+  // a per-FIFO stash (rq[16q+4] = count, rq[16q+5..] = chunks; one per warp
+  // slot, kept in global memory between launches), else the device-wide
+  // pool: a lock-free free stack of chunk chains (ABA tag in the high word),
+  // else never-used chunks (handed out kBump at a time).  Passed and
+  // released chunks go back to the stash, the overflow as ONE chain per
+  // release (they are linked already): the free-stack head is one hot word,
+  // so eviction-heavy runs (C4 rho >= 0.8, C5) must touch it rarely.
+  static constexpr uint32_t kStash = 11, kBump = 4;  // count + kStash = 12 words (3 x uint4)
   __device__ uint32_t pool_alloc(int q) const {
-    const uint32_t n = rq[8 * q + 4];
-    if (n) { rq[8 * q + 4] = n - 1; return rq[8 * q + 4 + n]; }
+    uint32_t* sq = rq + 16 * q;
+    const uint32_t n = sq[4];
+    if (n) { sq[4] = n - 1; return sq[4 + n]; }
     unsigned long long old = atomicAdd(P.pool_free, 0ull);
     while ((uint32_t)old != kNoChunk) {
       const uint32_t nxt = __ldcg(P.pool_next + (uint32_t)old);
@@ -442,86 +473,100 @@ struct WarpSim {
       if (prev == old) return (uint32_t)old;
       old = prev;
     }
-    const uint32_t c = atomicAdd(P.pool_bump, 1u);
-    return c < P.pool_chunks ? c : kNoChunk;
+    const uint32_t c = atomicAdd(P.pool_bump, kBump);
+    if (c >= P.pool_chunks) return kNoChunk;
+    // the rest of the batch goes to the stash (it is empty here)
+    const uint32_t extra = min(kBump, P.pool_chunks - c) - 1;
+    for (uint32_t i = 0; i < extra; ++i) sq[5 + i] = c + 1 + i;
+    sq[4] = extra;
+    return c;
   }
-  __device__ void pool_release(int q, uint32_t c) const {
-    const uint32_t n = rq[8 * q + 4];
-    if (n < kStash) { rq[8 * q + 5 + n] = c; rq[8 * q + 4] = n + 1; return; }
-    pool_push(c);
-  }
-  __device__ void pool_push(uint32_t c) const {
+  // push the chain first -> ... -> last (already linked) onto the free stack
+  __device__ void pool_push_chain(uint32_t first, uint32_t last) const {
     unsigned long long old = atomicAdd(P.pool_free, 0ull);
     for (;;) {
-      __stcg(P.pool_next + c, (uint32_t)old);
+      __stcg(P.pool_next + last, (uint32_t)old);
       __threadfence();
-      const unsigned long long nw = (((old >> 32) + 1ull) << 32) | c;
+      const unsigned long long nw = (((old >> 32) + 1ull) << 32) | first;
       const unsigned long long prev = atomicCAS(P.pool_free, old, nw);
       if (prev == old) return;
       old = prev;
     }
   }
+  // return the k linked chunks first -> ... (k >= 1) of FIFO q: to the stash
+  // while it has room, the rest as one chain
+  __device__ void pool_release_chain(int q, uint32_t first, uint32_t k) const {
+    uint32_t* sq = rq + 16 * q;
+    uint32_t n = sq[4];
+    while (k > 0 && n < kStash) {
+      sq[5 + n++] = first;
+      if (--k) first = __ldcg(P.pool_next + first);
+    }
+    sq[4] = n;
+    if (k == 0) return;
+    uint32_t last = first;
+    for (uint32_t i = 1; i < k; ++i) last = __ldcg(P.pool_next + last);
+    pool_push_chain(first, last);
+  }
   // pool entry of position pos (>= the committed head) of FIFO q
   __device__ __forceinline__ size_t fifo_entry(int q, uint32_t pos) const {
-    uint32_t c = rq[8 * q], ci = rq[8 * q + 1];
+    uint32_t c = rq[16 * q], ci = rq[16 * q + 1];
     for (const uint32_t want = pos / kRestartChunk; ci < want; ++ci) c = __ldcg(P.pool_next + c);
     return (size_t)c * kRestartChunk + pos % kRestartChunk;
   }
   // pool entry of tail position pos (the tail chunk or the one after it)
   __device__ __forceinline__ size_t fifo_wentry(int q, uint32_t pos) const {
-    uint32_t c = rq[8 * q + 2];
-    if (pos / kRestartChunk != rq[8 * q + 3]) c = __ldcg(P.pool_next + c);
+    uint32_t c = rq[16 * q + 2];
+    if (pos / kRestartChunk != rq[16 * q + 3]) c = __ldcg(P.pool_next + c);
     return (size_t)c * kRestartChunk + pos % kRestartChunk;
   }
   // lane q: chunks for cnt (<= 32) more entries at the tail t of FIFO q
   // (the chunk of the next write position included); false: pool exhausted
   __device__ bool fifo_reserve(int q, uint32_t t, uint32_t cnt) const {
-    if (rq[8 * q + 2] == kNoChunk) {
+    if (rq[16 * q + 2] == kNoChunk) {
       const uint32_t c = pool_alloc(q);
       if (c == kNoChunk) return false;
-      rq[8 * q] = rq[8 * q + 2] = c;
-      rq[8 * q + 1] = rq[8 * q + 3] = t / kRestartChunk;
+      rq[16 * q] = rq[16 * q + 2] = c;
+      rq[16 * q + 1] = rq[16 * q + 3] = t / kRestartChunk;
     }
-    if ((t + cnt) / kRestartChunk > rq[8 * q + 3]) {
+    if ((t + cnt) / kRestartChunk > rq[16 * q + 3]) {
       const uint32_t c = pool_alloc(q);
       if (c == kNoChunk) return false;
-      __stcg(P.pool_next + rq[8 * q + 2], c);
+      __stcg(P.pool_next + rq[16 * q + 2], c);
     }
     return true;
   }
   // lane q, after the writes: the tail chunk follows the new tail position
   __device__ void fifo_tail_done(int q, uint32_t t_new) const {
-    if (t_new / kRestartChunk > rq[8 * q + 3]) {
-      rq[8 * q + 2] = __ldcg(P.pool_next + rq[8 * q + 2]);
-      rq[8 * q + 3] += 1;
+    if (t_new / kRestartChunk > rq[16 * q + 3]) {
+      rq[16 * q + 2] = __ldcg(P.pool_next + rq[16 * q + 2]);
+      rq[16 * q + 3] += 1;
     }
   }
   // lane q: return the chunks the committed head has passed
   __device__ void fifo_commit(int q, uint32_t head) const {
-    while (rq[8 * q + 2] != kNoChunk && rq[8 * q + 1] < head / kRestartChunk) {
-      const uint32_t c = rq[8 * q];
-      rq[8 * q] = __ldcg(P.pool_next + c);
-      rq[8 * q + 1] += 1;
-      pool_release(q, c);
-    }
+    if (rq[16 * q + 2] == kNoChunk || rq[16 * q + 1] >= head / kRestartChunk) return;
+    const uint32_t first = rq[16 * q], k = head / kRestartChunk - rq[16 * q + 1];
+    uint32_t c = first;
+    for (uint32_t i = 0; i < k; ++i) c = __ldcg(P.pool_next + c);
+    rq[16 * q] = c;
+    rq[16 * q + 1] += k;
+    pool_release_chain(q, first, k);
   }
-  // lanes < n_rings: return the stashed chunks to the pool (kernel exit)
+  // lanes < n_rings: save the chunk stash of this slot (kernel exit)
   __device__ void flush_stash() const {
-    if (lane < P.n_rings)
-      for (uint32_t i = 0; i < rq[8 * lane + 4]; ++i) pool_push(rq[8 * lane + 5 + i]);
+    if (lane < P.n_rings) {
+      uint4* g = reinterpret_cast<uint4*>(P.pool_stash) + ((size_t)wslot * P.n_rings + lane) * 3;
+      const uint32_t* sq = rq + 16 * lane;
+      for (int i = 0; i < 3; ++i) g[i] = make_uint4(sq[4 + 4 * i], sq[5 + 4 * i], sq[6 + 4 * i], sq[7 + 4 * i]);
+    }
   }
   // lane q: return every chunk of FIFO q (end of the replication)
   __device__ void fifo_release_all(int q) const {
-    if (rq[8 * q + 2] == kNoChunk) return;
-    uint32_t c = rq[8 * q];
-    for (;;) {
-      const uint32_t nxt = __ldcg(P.pool_next + c);
-      const bool last = c == rq[8 * q + 2];
-      pool_release(q, c);
-      if (last) break;
-      c = nxt;
-    }
-    rq[8 * q] = rq[8 * q + 2] = kNoChunk;
+    if (rq[16 * q + 2] == kNoChunk) return;
+    const uint32_t k = rq[16 * q + 3] - rq[16 * q + 1] + 1;  // head chunk .. tail chunk
+    pool_release_chain(q, rq[16 * q], k);
+    rq[16 * q] = rq[16 * q + 2] = kNoChunk;
   }
   // NESTED stage info: segment index (bits 0-5), last stage of the segment
   // (bit 6), entry stage (bit 7); counter slot = segment (+32 at entry)
@@ -1250,78 +1295,50 @@ struct WarpSim {
   }
 
   // S4 for the class-ring engine: LIFO eviction of up
-  // to 32 victims per round.  The newest residents are the class-ring tails;
-  // each tail record's LIFO rank = its depth in its own ring + the number of
-  // newer (larger sequence number) tail records of the other classes, by
-  // binary search; then an inclusive scan of freed KV finds the cut.
-  __device__ __forceinline__ uint32_t ring_tail_idx(uint32_t off, uint32_t head, uint32_t n, uint32_t cap,
-                                                    uint32_t j) const {
-    return off + wrap(head + (n - 1 - j), cap);  // j-th newest resident of a class
-  }
+  // to 32 victims per round.  The admission log (global, one class byte per
+  // admission in admission order, truncated by evictions) gives the LIFO
+  // order across classes: the log entries of class c are its completed
+  // members (oldest) followed by its r_n residents, so the j-th newest
+  // class-c entry is resident iff j < r_n, at ring position tail - 1 - j.
+  // A round reads the 32 newest entries, loads the residents' records, and
+  // an inclusive scan of freed KV finds the cut; everything newer than the
+  // cut leaves the log.
   __device__ void memory_ring(uint32_t& n_evict, int64_t& peak) {
     peak = KV + (int64_t)n_plan_res + sum_new_l;
     if (peak <= P.M) return;
     int64_t excess = peak - P.M;
     const int K = P.K;
-    // victims of a round are staged after the admissions: up to 32, at least
-    // the P.spare slots beyond the staging capacity
-    const uint32_t vcap = min(32u, P.Rc + P.spare - n_new);
+    const uint8_t* log = P.ring_log + (size_t)wslot * kRingLog;
     while (excess > 0 && n_res > 0) {
-      const uint32_t nc = lane < K ? min(r_n, vcap) : 0u;  // class `lane`'s tail window
-      const uint32_t incl = warp_incl_scan_u32(nc, lane);
-      const uint32_t ncand = __shfl_sync(FULL, incl, 31);
-      const uint32_t my_off = lane < K ? P.roff[lane] : 0u, my_cap = lane < K ? P.rcap[lane] : 1u;
-      // (1) rank every tail-window record; rank < 32 -> victim slot
-      for (uint32_t g0 = 0; g0 < ncand; g0 += 32) {
-        const uint32_t g = g0 + (uint32_t)lane;
-        const bool act = g < ncand;
-        int sc = 0;
-        for (int c = 0; c < K; ++c) sc += bcast32(incl, c) <= g;
-        sc = min(sc, K - 1);
-        const uint32_t j = g - (__shfl_sync(FULL, incl, sc) - __shfl_sync(FULL, nc, sc));
-        const uint32_t idx = ring_tail_idx(__shfl_sync(FULL, my_off, sc), __shfl_sync(FULL, r_head, sc),
-                                           __shfl_sync(FULL, r_n, sc), __shfl_sync(FULL, my_cap, sc), j);
-        RRec e = {0, 0, 0};
-        if (act) e = rg[idx];
-        uint32_t r = j;
-        for (int c = 0; c < K; ++c) {
-          const uint32_t n = bcast32(nc, c);
-          const uint32_t off = bcast32(my_off, c), head = bcast32(r_head, c), rn = bcast32(r_n, c),
-                         cap = bcast32(my_cap, c);  // (all lanes: shuffles before any divergence)
-          if (!act || c == sc || n == 0) continue;
-          uint32_t lo = 0, len = n;  // # of class-c tail records newer than e
-          while (len > 0) {
-            const uint32_t half = len >> 1;
-            if (rg[ring_tail_idx(off, head, rn, cap, lo + half)].seq > e.seq) { lo += half + 1; len -= half + 1; }
-            else len = half;
-          }
-          r += lo;
-        }
-        __syncwarp();
-        if (act && r < vcap) { rr[sbase() + n_new + r] = Rec{e.a, (uint64_t)e.xf | ((uint64_t)sc << 32)}; }
-        __syncwarp();
-      }
-      // (2) victims in LIFO order: lane r holds the r-th newest resident
-      const uint32_t nv = min(ncand, vcap);
-      const bool valid = (uint32_t)lane < nv;
-      Rec e = {0, 0};
-      if (valid) e = rr[sbase() + n_new + lane];
-      const uint32_t xf = (uint32_t)e.q, v = (uint32_t)(e.q >> 32) & 31u;
-      const uint32_t x = xf & XF_X, Cv = __shfl_sync(FULL, r_C, (int)v);
+      const uint32_t lo = seq_max > kRingLog ? seq_max - kRingLog : 0u;  // oldest entry still in the log
+      if (seq_next <= lo) { status = 1; return; }                       // log window exhausted
+      const uint32_t avail = min(seq_next - lo, 32u);
+      const bool valid = (uint32_t)lane < avail;
+      const uint32_t pos = seq_next - 1 - (uint32_t)lane;  // lane 0 = the newest admission
+      const uint32_t v = valid ? (uint32_t)__ldcg(log + (pos & (kRingLog - 1))) : 0u;
+      const uint32_t grp = __match_any_sync(FULL, valid ? v : 0x100u + (uint32_t)lane);
+      const uint32_t j = __popc(grp & lanemask_lt());  // class-v entries newer than this one
+      const uint32_t rn = __shfl_sync(FULL, r_n, (int)v), head = __shfl_sync(FULL, r_head, (int)v);
+      const uint32_t Cv = __shfl_sync(FULL, r_C, (int)v), Rv = __shfl_sync(FULL, r_Ri, (int)v);
+      const bool res = valid && j < rn;
+      RRec e = {0, 0, 0};
+      if (res) e = rg[P.roff[v] + wrap(head + (rn - 1 - j), P.rcap[v])];
+      const uint32_t xf = e.xf, x = xf & XF_X;
       const uint32_t fl = P.fl[v], l = fl & 0xFFFFu, lp = fl >> 16;
       const uint32_t s = Cv - x;  // next stage to run
-      const uint32_t inp = valid && (POL == SCHED_WAIT ? ((Qmask >> v) & 1u) : 1u);
-      const uint32_t f = valid ? (l + s - 1 + inp) : 0u;
+      const uint32_t inp = res && (POL == SCHED_WAIT ? ((Qmask >> v) & 1u) : 1u);
+      const uint32_t f = res ? (l + s - 1 + inp) : 0u;
       const uint32_t cum = warp_incl_scan_u32(f, lane);
-      const uint32_t hit = __ballot_sync(FULL, valid && (int64_t)cum >= excess);
-      const uint32_t ne = hit ? (uint32_t)__ffs(hit) : nv;
-      const bool ev = (uint32_t)lane < ne;
+      const uint32_t hit = __ballot_sync(FULL, res && (int64_t)cum >= excess);
+      const uint32_t ntr = hit ? (uint32_t)__ffs(hit) : avail;  // log entries removed
+      const bool ev = res && (uint32_t)lane < ntr;
+      const uint32_t ne = __popc(__ballot_sync(FULL, ev));
       // a first token still pending (admitted at the last participation) was not emitted
       const bool pend = ev && (xf & XF_PEND) && x == Cv - 1;
       // restart records in eviction order (re-enter the queue)
       const int q = POL == SCHED_WAIT ? (int)v : 0;
-      const uint32_t grp = __match_any_sync(FULL, ev ? (uint32_t)q : (0x100u + (uint32_t)lane));
-      const uint32_t before = __popc(grp & lanemask_lt());
+      const uint32_t gq = __match_any_sync(FULL, ev ? (uint32_t)q : (0x100u + (uint32_t)lane));
+      const uint32_t before = __popc(gq & lanemask_lt());
       const uint32_t tail_q = __shfl_sync(FULL, rtail, q);
       uint32_t my_cnt = POL == SCHED_WAIT ? 0u : (lane == 0 ? ne : 0u);
       if (POL == SCHED_WAIT)
@@ -1342,6 +1359,9 @@ struct WarpSim {
         P.pool_llp[ri] = v | (((xf & XF_FT) && !pend) ? 0x80000000u : 0u);
         sh_add_u32(&cnt[v], 1u);
         sh_add_u64(&xs[v], (uint64_t)x);
+        acc_ev += (uint64_t)e.a;
+        // the victim leaves its cohort (stage s = C - x in 1..l')
+        sh_add_u32(&coh[P.ccoff[v] + (Rv >= s ? Rv - s : Rv + lp + 1 - s)], ~0u);
         if (pend) { sh_add_u32(&cnt[32 + v], ~0u); sh_add_u64(&psum()[v], (uint64_t)(-e.a)); }
       }
       __syncwarp();
@@ -1357,12 +1377,12 @@ struct WarpSim {
       n_plan_res -= __reduce_add_sync(FULL, ev ? inp : 0u);
       n_res -= ne;
       n_evict += ne;
+      seq_next -= ntr;
       __syncwarp();
     }
     if (excess > 0) drop_admissions(excess);
     peak = P.M + excess;
   }
-
 
   // ====================================== S4/S5, NESTED segment engine (SEG)
   // Every prompt passes the stages in admission order: an entry stage takes
@@ -1903,10 +1923,13 @@ struct WarpSim {
     uint32_t tok, nd, nf, dtok, kvf, gr;
     uint64_t done_a = 0, ft_a = 0;
     if (RING) {
-      ring_pass(tok, nd, nf, dtok, kvf, done_a, ft_a);
+      ring_pass(tok, nd, nf, dtok, kvf, ft_a);
       gr = n_plan_res - nd;
       if (!ring_append()) return;
-      if (lane < P.K && (POL == SCHED_WAIT ? ((Qmask >> lane) & 1u) : 1u)) ++r_C;
+      if (lane < P.K && (POL == SCHED_WAIT ? ((Qmask >> lane) & 1u) : 1u)) {
+        ++r_C;
+        r_Ri = r_Ri == (P.fl[lane] >> 16) ? 0u : r_Ri + 1;
+      }
       n_res = n_res - nd + n_new;
     } else {
       member_pass(tok, nd, nf, dtok, kvf, gr, done_a, ft_a);
@@ -1915,53 +1938,51 @@ struct WarpSim {
   }
 
   // S5 for the class-ring engine: the stage of a member admitted at class
-  // clock x is C_c - x, so the stage-l' completions are a prefix of ring c
-  // and the stage-1 first tokens are
-  // the prompts admitted at the class's previous participation without one
-  // (counted at append); plan tokens sum_(l + s) = n_c (l_c + C_c) - sum x
+  // clock x is C_c - x, so the stage-l' completions
+  // are the cohort admitted at x = C_c - l' (a count per clock slot) and
+  // the stage-1 first tokens the prompts admitted at the
+  // class's previous participation without one (counted at append); plan
+  // tokens sum_(l + s) = n_c (l_c + C_c) - sum x.  O(K) per batch: no
+  // member record is read (the arrival ticks of completions enter the
+  // latency sum through admitted - evicted - late - still resident).
   __device__ void ring_pass(uint32_t& tok, uint32_t& nd, uint32_t& nf, uint32_t& dtok, uint32_t& kvf,
-                            uint64_t& done_a, uint64_t& ft_a) {
+                            uint64_t& ft_a) {
     const bool cin = lane < P.K && (POL == SCHED_WAIT ? ((Qmask >> lane) & 1u) : 1u);
     const uint32_t fl = lane < P.K ? P.fl[lane] : 0u, l = fl & 0xFFFFu, lp = fl >> 16;
     const uint32_t tk = cin ? (uint32_t)((uint64_t)r_n * (l + r_C) - r_X) : 0u;
+    tok = __reduce_add_sync(FULL, tk);
     uint32_t my_nd = 0, my_nf = 0;
     if (cin) {  // stage-1 members emit their first token
       my_nf = cnt[32 + lane];
       ft_a += psum()[lane];
       cnt[32 + lane] = 0;
       psum()[lane] = 0;
+      // the cohort x = C - l' runs its last stage (slot (C + 1) mod (l' + 1))
+      const uint32_t i = P.ccoff[lane] + (r_Ri == lp ? 0u : r_Ri + 1);
+      my_nd = coh[i];
+      coh[i] = 0;
     }
-    uint32_t cm = __ballot_sync(FULL, cin && r_n > 0);
-    while (cm) {
-      const int c = __ffs(cm) - 1;
-      cm &= cm - 1;
-      const uint32_t n = bcast32(r_n, c), head = bcast32(r_head, c), C = bcast32(r_C, c);
-      const uint32_t cap = P.rcap[c], lpc = P.fl[c] >> 16;
-      const RRec* R = rg + P.roff[c];
-      // completions: stage-l' members (x = C - l') from the head
-      uint32_t ndc = 0;
-      if (C >= lpc) {
-        for (uint32_t j0 = 0; j0 < n; j0 += 32) {
-          const uint32_t j = j0 + (uint32_t)lane;
-          bool dn = false;
-          if (j < n) {
-            const RRec* e = R + wrap(head + j, cap);
-            dn = (e->xf & XF_X) == C - lpc;
-            if (dn) done_a += (uint64_t)e->a;
-          }
-          const uint32_t m = __ballot_sync(FULL, dn);
-          ndc += __popc(m);
-          if (m != FULL) break;
+    // a batch ending after T is the last one; its completions are not
+    // counted (A19): their arrival ticks leave the completion sum here
+    {
+      const int64_t tokens = (int64_t)tok + sum_new_l;
+      const int64_t tau = P.d0_t + P.d1_t * max(tokens - P.b0, (int64_t)0);
+      if (now + tau > P.T_t) {
+        u128 al = 0;
+        for (uint32_t cm = __ballot_sync(FULL, my_nd > 0); cm; cm &= cm - 1) {
+          const int c = __ffs(cm) - 1;
+          const uint32_t n = bcast32(my_nd, c), head = bcast32(r_head, c), cap = P.rcap[c];
+          for (uint32_t j = lane; j < n; j += 32) al += (uint64_t)rg[P.roff[c] + wrap(head + j, cap)].a;
         }
-      }
-      if (lane == c) {
-        my_nd = ndc;
-        r_head = wrap(r_head + ndc, cap);
-        r_n -= ndc;
-        r_X -= (uint64_t)ndc * (C - lpc);
+        al = warp_sum_u128(al);
+        if (lane == 0) st->acc_ev += al;
       }
     }
-    tok = __reduce_add_sync(FULL, tk);
+    if (cin) {
+      r_head = wrap(r_head + my_nd, P.rcap[lane]);
+      r_n -= my_nd;
+      r_X -= (uint64_t)my_nd * (r_C - lp);
+    }
     nd = __reduce_add_sync(FULL, my_nd);
     nf = __reduce_add_sync(FULL, my_nf);
     dtok = __reduce_add_sync(FULL, my_nd * lp);
@@ -1970,9 +1991,10 @@ struct WarpSim {
   }
 
   // append the staged admissions (stage 1 next, admission clock = C_c) to
-  // their class rings, in admission order; false on ring overflow (status 1:
-  // the replication is re-run with the safe capacity)
+  // their class rings (global memory), in admission order; cohort counts of
+  // the current clocks; false on ring overflow (status 1)
   __device__ bool ring_append() {
+    uint32_t my_new = 0;
     for (uint32_t j0 = 0; j0 < n_new; j0 += 32) {
       const uint32_t j = j0 + (uint32_t)lane;
       const bool v = j < n_new;
@@ -1981,7 +2003,8 @@ struct WarpSim {
       const uint32_t meta = (uint32_t)(e.q >> 48), c = v ? (meta & 0xFFu) : 0u;
       const uint32_t grp = __match_any_sync(FULL, v ? c : 0x100u + (uint32_t)lane);
       const uint32_t rk = __popc(grp & lanemask_lt());
-      const uint32_t n = __shfl_sync(FULL, r_n, (int)c), head = __shfl_sync(FULL, r_head, (int)c);
+      const uint32_t n = __shfl_sync(FULL, r_n, (int)c) + __shfl_sync(FULL, my_new, (int)c);
+      const uint32_t head = __shfl_sync(FULL, r_head, (int)c);
       const uint32_t C = __shfl_sync(FULL, r_C, (int)c), cap = P.rcap[c];
       if (__any_sync(FULL, v && n + rk >= cap)) { status = 1; return false; }
       cnt[lane] = 0;
@@ -1990,6 +2013,8 @@ struct WarpSim {
       const bool pend = v && !(meta & META_FT);
       if (v) {
         rg[P.roff[c] + wrap(head + n + rk, cap)] = RRec{e.a, C | XF_FT | (pend ? XF_PEND : 0u), seq_next + j};
+        P.ring_log[(size_t)wslot * kRingLog + ((seq_next + j) & (kRingLog - 1))] = (uint8_t)c;
+        acc_adm += (uint64_t)e.a;
         if (rk == 0) cnt[c] = __popc(grp);
       }
       if (pend) {  // per-class pending first tokens (shared: pcnt = cnt[32..], psum)
@@ -1997,15 +2022,31 @@ struct WarpSim {
         sh_add_u64(&psum()[c], (uint64_t)e.a);
       }
       __syncwarp();
-      if (lane < P.K) {
-        const uint32_t k = cnt[lane];
-        r_n += k;
-        r_X += (uint64_t)k * r_C;
-      }
+      if (lane < P.K) my_new += cnt[lane];
       __syncwarp();
     }
+    if (lane < P.K) {
+      r_n += my_new;
+      r_X += (uint64_t)my_new * r_C;
+      coh[P.ccoff[lane] + r_Ri] += my_new;
+    }
     seq_next += n_new;
+    seq_max = max(seq_max, seq_next);
     return true;
+  }
+
+  // end of a replication (RING): arrival-tick sum of the residents still in
+  // the class rings, so that the completion sum is admitted - evicted -
+  // late - resident
+  __device__ void ring_finish() {
+    u128 ar = 0;
+    for (int c = 0; c < P.K; ++c) {
+      const uint32_t n = bcast32(r_n, c), head = bcast32(r_head, c), cap = P.rcap[c];
+      for (uint32_t j = lane; j < n; j += 32) ar += (uint64_t)rg[P.roff[c] + wrap(head + j, cap)].a;
+    }
+    ar = warp_sum_u128(ar);
+    if (lane == 0) st->acc_done_a = st->acc_adm - st->acc_ev - ar;
+    __syncwarp();
   }
 
   // S5 for the member engine: one pass over residents (+ the staged
@@ -2150,12 +2191,18 @@ struct WarpSim {
     }
     __syncwarp();
     k_vis = vbase = k_adm = abase = pcount = rhead = rtail = 0;
-    if (lane < P.n_rings) rq[8 * lane] = rq[8 * lane + 2] = kNoChunk;
+    if (lane < P.n_rings) rq[16 * lane] = rq[16 * lane + 2] = kNoChunk;
     vprev = aprev = 0;
     newc = 0;
     r_head = r_n = r_C = seq_next = 0;
+    r_Ri = 0;
+    seq_max = 0;
     r_X = 0;
-    if (RING) psum()[lane] = 0;
+    if (RING) {
+      psum()[lane] = 0;
+      acc_adm = acc_ev = 0;
+      for (uint32_t i = lane; i < P.ccsize; i += 32) coh[i] = 0;
+    }
     if (SEG) {
       head = tail = 0;
       pf_n = 0; pf_a = 0;
@@ -2208,6 +2255,7 @@ struct WarpSim {
     flush_acc();
     __syncwarp();
     if (SEG) seg_finish();
+    if (RING) ring_finish();
     const WarpStats S = *st;
     const uint64_t arrivals = S.arrivals, completed = S.completed;
     const u128 lat = S.sum_done_t - S.acc_done_a;
