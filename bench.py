@@ -569,6 +569,8 @@ def main():
     ap.add_argument("--ref-reps", type=int, default=64)
     ap.add_argument("--cpu-reps", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", default="auto", choices=["auto", "serial", "concurrent"],
+                    help="policy launches on one stream or one stream each (auto: serial when each fills >= 2 waves)")
     ap.add_argument("--no-extra", action="store_true", help="skip the C3a Nested block of the default line")
     ap.add_argument("--total", type=int, default=0,
                     help="strong scaling (C4): replications per (rho, policy) point, sharded over ranks")
@@ -618,6 +620,8 @@ def main():
         return n / max(1, li["grid"] * li["warps_per_block"])
     n_local = D.rep_range(0, rank, world, R)[1]
     serial = all(waves(s, n_local) >= 2.0 for _, s, _ in scheds)
+    if args.streams != "auto":
+        serial = args.streams == "serial"
     pstreams = [torch.cuda.Stream(dev)] * len(scheds) if serial else [torch.cuda.Stream(dev) for _ in scheds]
 
     def step(k, ev_start=None, ev_ends=None, ev_begins=None):

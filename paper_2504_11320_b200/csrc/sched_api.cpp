@@ -288,7 +288,7 @@ int prepare(sched_s* h) {
     int best_w = 0;
     const int cands[] = {8, 4, 2, 1};
     for (int wpb : cands) {
-      if (h->in.policy == SCHED_WAIT && wpb > 4) continue;  // kernel launch bound: 128 threads
+      if ((h->in.policy == SCHED_WAIT || ring) && wpb > 4) continue;  // kernel launch bound: 128 threads
       const size_t smem = (size_t)wpb * *wsm;
       if (smem > (size_t)prop.sharedMemPerBlockOptin) continue;
       // max blocks per SM from shared memory and registers (occupancy API)

@@ -2298,9 +2298,12 @@ struct WarpSim {
 };
 
 template <int POL, bool TRACE, bool RING, bool SEG>
-// WAIT: <= 4 warps per block, 5 blocks per SM -> <= 102 registers (20 warps/SM
-// at C2's shared-memory footprint); others are shared-memory bound: 128 regs
-__global__ void __launch_bounds__(POL == SCHED_WAIT ? 128 : 256, POL == SCHED_WAIT ? 5 : 2)
+// WAIT and the class-ring engine: <= 4 warps per block, 5 blocks per SM ->
+// <= 102 registers, 20 warps/SM (the ring engine's shared footprint is small,
+// so registers bound its occupancy: measured C2 FCFS 128 registers / 16
+// warps 20.9 ms -> 96 / 20 warps 18.7 ms; 80 / 24 warps spills, 20.7 ms);
+// the member and segment engines are shared-memory bound: 128 registers
+__global__ void __launch_bounds__((POL == SCHED_WAIT || RING) ? 128 : 256, (POL == SCHED_WAIT || RING) ? 5 : 2)
     sim_kernel(const DevParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int wib = threadIdx.x >> 5;
