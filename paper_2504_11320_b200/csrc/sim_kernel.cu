@@ -348,7 +348,7 @@ struct WarpSim {
   // tick of arrival (base - 1), the scan carry.
   uint32_t k_vis, vbase, k_adm, abase, pcount, rhead, rtail;
   int64_t vprev, aprev;
-  uint32_t sv_k, sv_rhead;           // saved admission cursor (drop/rewind)
+  uint32_t sv_k, sv_rhead, sv_have;  // saved admission cursor (drop/rewind); sv_prev valid
   int64_t sv_prev;
   uint32_t newc;                     // WAIT: admissions of class `lane` this epoch
 
@@ -803,7 +803,7 @@ struct WarpSim {
     sum_new_l += __reduce_add_sync(FULL, (uint32_t)lane < take ? l : 0u);
     want -= take;
     __syncwarp();
-    return take < m ? 0 : 1;
+    return take < m ? 0 : m < p ? 1 : 2;
   }
 
   // take_fifo fast path, several classes merged by (t, class): candidate g
@@ -859,7 +859,7 @@ struct WarpSim {
     sum_new_l += __reduce_add_sync(FULL, tk ? l : 0u);
     want -= take;
     __syncwarp();
-    return take < m ? 0 : 1;
+    return take < m ? 0 : m < ncand ? 1 : 2;
   }
 
   // take_merged for KK <= 4 classes: each class's candidates (lane i = its
@@ -883,6 +883,28 @@ struct WarpSim {
     if (m == 0) return 0;
     if (base + m > P.Rc) { status = 1; return -1; }
     const uint32_t i = (uint32_t)lane;
+    if (KK == 2) {
+      // lane i holds both classes' i-th candidates; each candidate's rank
+      // i + #(earlier arrivals of the other class) by a branch-free binary
+      // search over the other class's ticks held in lanes (shuffles; ties
+      // to class 0)
+      uint32_t i0 = 0, i1 = 0;
+      int64_t t0 = TMAX, t1 = TMAX;
+      if (i < n[0]) { i0 = sg[0].at(i); t0 = vt[i0]; }
+      if (i < n[1]) { i1 = sg[1].at(i); t1 = vt[i1]; }
+      uint32_t r0 = 0, r1 = 0;  // # of class-1 ticks < t0, # of class-0 ticks <= t1
+#pragma unroll
+      for (uint32_t step = 32; step >= 1; step >>= 1) {
+        const int64_t x1 = __shfl_sync(FULL, t1, (int)((r0 + step - 1) & 31u));
+        const int64_t x0 = __shfl_sync(FULL, t0, (int)((r1 + step - 1) & 31u));
+        if (r0 + step <= n[1] && x1 < t0) r0 += step;
+        if (r1 + step <= n[0] && x0 <= t1) r1 += step;
+      }
+      r0 += i;
+      r1 += i;
+      if (i < n[0] && r0 < m) rr[base + r0] = Rec{t0, pack_q(vl[i0], vlp[i0], 1, 0u)};
+      if (i < n[1] && r1 < m) rr[base + r1] = Rec{t1, pack_q(vl[i1], vlp[i1], 1, 1u)};
+    } else {
 #pragma unroll
     for (int src = 0; src < KK; ++src) {
       if (i < n[src] && i < m) {
@@ -903,6 +925,7 @@ struct WarpSim {
         if (r < m) rr[base + r] = Rec{t, pack_q(vl[idx], vlp[idx], 1, (uint32_t)src)};
       }
     }
+    }
     __syncwarp();
     uint64_t qv = 0;
     uint32_t l = 0;
@@ -920,7 +943,7 @@ struct WarpSim {
     sum_new_l += __reduce_add_sync(FULL, tk ? l : 0u);
     want -= take;
     __syncwarp();
-    return take < m ? 0 : 1;
+    return take < m ? 0 : m < ncand ? 1 : 2;
   }
 
   template <bool FCFS_COND>
@@ -951,10 +974,13 @@ struct WarpSim {
         }
         if (__all_sync(FULL, ok)) {
           const Seg sg{o1, len1, o2};
+          // every waiting arrival was offered (no class beyond 32): taking
+          // all of them ends the admissions
+          const bool capped = __any_sync(FULL, pend > 32u);
           if (c_hi - c_lo == 1) {
             const int r = take_single<FCFS_COND>(c_lo, min(pend, 32u), sg, want);
             if (r < 0) return false;
-            if (r == 0) break;
+            if (r == 0 || (r == 2 && !capped)) break;
             continue;
           }
           // FCFS admits whole chunks: per-class ranking wins for K <= 4
@@ -966,7 +992,7 @@ struct WarpSim {
                       : P.K == 4 ? take_merged_k<FCFS_COND, 4>(pc, sg, want)
                                  : take_merged<FCFS_COND>(pc, sg, want);
           if (r < 0) return false;
-          if (r == 0) break;
+          if (r == 0 || (r == 2 && !capped)) break;
           continue;
         }
       }
@@ -995,6 +1021,7 @@ struct WarpSim {
           if (n1 + n2 < min(p, min(want, 32u))) {
             // backlog deeper than the windows: regenerate the private window
             const int64_t prev = carry_before(c, ka);
+            if (lane == c) save_carry();  // before the saved cursor's carry can leave the windows
             fill<true>(c, ka, prev, at, al, alp);
             if (lane == c) { abase = ka; aprev = prev; pcount = 32; }
             o1 = 0;
@@ -1110,20 +1137,31 @@ struct WarpSim {
   }
 
   // save / restore the admission cursors (rare: a drop after eviction)
+  // (the scan carry of the saved cursor is read lazily: only a private-
+  // window regeneration during the takes, or a restore, needs it)
   __device__ void save_cursors() {
     sv_k = k_adm;
     sv_rhead = rhead;
-    sv_prev = 0;
-    if (lane < P.K && k_adm > 0) {  // scan carry of arrival k_adm - 1 of class `lane`
-      const bool tv = is_tv(lane);
-      if (k_adm > vbase) sv_prev = (tv ? vtau : vt)[lane * 32 + (k_adm - 1 - vbase)];
-      else if (k_adm == vbase) sv_prev = vprev;
-      else if (k_adm > abase) sv_prev = (tv ? atau : at)[lane * 32 + (k_adm - 1 - abase)];
-      else sv_prev = aprev;
-    }
+    sv_have = 0;
     newc = 0;
   }
+  // lane < K: the scan carry of arrival sv_k - 1 of class `lane` from the
+  // windows (unchanged since save_cursors unless sv_have)
+  __device__ void save_carry() {
+    if (lane < P.K && !sv_have) {
+      sv_prev = 0;
+      if (sv_k > 0) {
+        const bool tv = is_tv(lane);
+        if (sv_k > vbase) sv_prev = (tv ? vtau : vt)[lane * 32 + (sv_k - 1 - vbase)];
+        else if (sv_k == vbase) sv_prev = vprev;
+        else if (sv_k > abase) sv_prev = (tv ? atau : at)[lane * 32 + (sv_k - 1 - abase)];
+        else sv_prev = aprev;
+      }
+      sv_have = 1;
+    }
+  }
   __device__ void restore_cursors() {
+    save_carry();
     for (int c = 0; c < P.K; ++c) {
       const uint32_t k = bcast32(sv_k, c);
       const int64_t pv = bcast64(sv_prev, c);
