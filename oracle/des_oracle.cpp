@@ -323,7 +323,14 @@ struct Sim {
   // a correct simulator: the tests require status 0).
   uint64_t& q_at(const Prompt& p) { return qcnt[(S.policy == ORC_WAIT ? p.c : 0) * qw + p.s]; }
   void clear_q() { for (const Prompt& p : res) q_at(p) = 0; }
+  //
+  // Nested also checks the ordering property the CUDA segment engine relies
+  // on (derived from the same two rules: every non-entry
+  // stage of an active segment advances, an entry stage takes its oldest
+  // n_k first): residents in admission order have
+  // non-increasing stages.  A violation is status 3 as well.
   void check_p14() {
+    int prev_s = INT32_MAX;
     for (const Prompt& p : res) {
       if (S.policy == ORC_WAIT) {
         if (++q_at(p) > S.thr[p.c]) status = 3;
@@ -331,6 +338,8 @@ struct Sim {
         const int k = segment_of(p.s);
         const bool entry = k >= 1 && p.s == S.seg_end[k - 1] + 1;
         if (!entry && ++q_at(p) > S.thr[k]) status = 3;
+        if (p.s > prev_s) status = 3;
+        prev_s = p.s;
       }
     }
     clear_q();

@@ -671,6 +671,35 @@ def test_p14_stage_counts_never_exceed_thresholds():
         assert rows[F["batches"]].min() > 20
 
 
+def test_nested_admission_order_is_stage_order():
+    """The ordering the CUDA segment engine is built on:
+    under Algorithm 2 (every non-entry stage of an active
+    segment advances, an entry stage takes its oldest n_k first, R6) and
+    LIFO eviction, residents in admission order have
+    non-increasing stages at every decision epoch -- the oracle flags a
+    violation with status 3.  Exercised on strict and paper thresholds,
+    thrashing overload (C5 at 110 QPS with the paper's 66:43:... ratios:
+    ~3e6 evictions), one-stage segments, marks and random small systems."""
+    seg10 = [50 * k for k in range(1, 11)]
+    cases = [(W.C3A, [20, 40, 80, 160], W.PAPER_NESTED_RATIO_C3A, 10.0),
+             (W.c5(110.0), seg10, W.PAPER_NESTED_RATIO_C5, 60.0),
+             (W.c4(4), [100, 200, 300], [7, 5, 2], 5.0),
+             (W.Workload("w0", [30.0, 20.0], [W.fixed(3), [(1, 2), (6, 1)]],
+                         [[(2, 1), (3, 1), (4, 2)], W.fixed(5)], M=90, horizon_s=3.0, seed=123,
+                         d0_s=0.01, d1_s=1e-4), [2, 3, 4, 5], [3, 3, 2, 2], None)]
+    rng = np.random.default_rng(77)
+    for _ in range(12):
+        wl = W.random_small(rng, horizon_s=1.5)
+        maxlp = max(v for t in wl.lp_tab for v, _ in t)
+        seg = sorted({int(x) for x in rng.integers(1, maxlp + 1, 3)} | {maxlp})
+        cases.append((wl, seg, sorted([int(x) for x in rng.integers(1, 6, len(seg))], reverse=True), None))
+    for wl, seg, thr, T in cases:
+        rows = oracle.run(wl, W.Policy(W.NESTED, seg_end=seg), thr, n_reps=6, n_threads=6, horizon_s=T)
+        assert (rows[F["status"]] == 0).all(), wl.name
+    assert int(oracle.run(W.c5(110.0), W.Policy(W.NESTED, seg_end=seg10), W.PAPER_NESTED_RATIO_C5, n_reps=1,
+                          horizon_s=60.0)[F["evictions"]][0]) > 100_000
+
+
 # ------------------------------------------------- P17 Kingman, P19 Thm 2
 def test_p17_kingman_queue_bounds():
     """P17: the mean post-service queue at batch epochs, (sum_waiting -

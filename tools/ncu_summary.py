@@ -62,10 +62,14 @@ for r in rows[2:]:
         u = units[idx[key]]
         return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
     try:
-        traffic[short] = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
+        # one entry per policy: the longest launch (the main launch, not its
+        # empty speculative-capacity fallback)
+        dur = num("gpu__time_duration.sum")
+        if short not in traffic or dur > traffic[short][1]:
+            traffic[short] = (num("dram__bytes_read.sum") + num("dram__bytes_write.sum"), dur)
     except (KeyError, ValueError):
         pass
 open(out, "w").write("\n".join(lines) + "\n")
 if traffic_path:
-    json.dump(traffic, open(traffic_path, "w"), indent=1)
+    json.dump({k: v[0] for k, v in traffic.items()}, open(traffic_path, "w"), indent=1)
 print("\n".join(lines))

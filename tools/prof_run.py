@@ -25,15 +25,15 @@ elif wl_name == "C3a_tv":
 elif wl_name == "C3b":
     wl, pols = W.C3B, [W.Policy(W.NESTED, seg_end=seg10), W.Policy(W.FCFS, B=2048)]
 else:
-    wl, pols = W.c5(55.0), [W.Policy(W.NESTED, seg_end=seg10, thresholds=W.PAPER_NESTED_RATIO_C5),
-                            W.Policy(W.FCFS, B=1024)]
+    wl, pols = W.c5(55.0), [W.Policy(W.NESTED, seg_end=seg10), W.Policy(W.FCFS, B=1024)]  # bench.py's C5
 if os.environ.get("POLS"):
     keep = os.environ["POLS"].split(",")
     pols = [p for p in pols if W.POLICY_NAMES[p.kind] in keep]
 R = int(os.environ.get("REPS", "10000"))
 T = float(os.environ.get("HORIZON", str(wl.horizon_s)))
 for pol in pols:
-    s = Scheduler(wl, pol, pol.thresholds)
+    kw = dict(max_resident=4096, restart_cap=2_000_000_000) if wl_name.startswith("C5") else {}
+    s = Scheduler(wl, pol, pol.thresholds, **kw)
     if pol.kind != W.FCFS and not pol.thresholds:
         s.thresholds()
     rows = run_rows(s, wl.seed, 0, R, T)

@@ -1,5 +1,5 @@
-"""Write the round's profiles/ summaries from a measurement pass (tools/gpu_measure.sh).
-usage: python tools/write_profiles.py TAG"""
+"""Write the round's profiles/ summaries from a measurement pass (tools/gpu_measure_r2.sh).
+usage: python tools/write_profiles.py TAG [ROUND_PREFIX=r2]"""
 import collections
 import csv
 import json
@@ -8,19 +8,20 @@ import subprocess
 import sys
 
 tag = sys.argv[1]
+R = sys.argv[2] if len(sys.argv) > 2 else "r2"
 G = "gpurun_out/"
 # bench matrix
 lines = [json.loads(l) for l in open(G + "bench_matrix.jsonl")]
-shutil.copy(G + "bench_matrix.jsonl", "profiles/r1_bench_matrix.jsonl")
-shutil.copy(G + "bench_reference.json", "profiles/r1_bench_reference.json")
-shutil.copy(G + "bench_default.json", "profiles/r1_bench_c2_default.json")
+shutil.copy(G + "bench_matrix.jsonl", f"profiles/{R}_bench_matrix.jsonl")
+shutil.copy(G + "bench_reference.json", f"profiles/{R}_bench_reference.json")
+shutil.copy(G + "bench_default.json", f"profiles/{R}_bench_c2_default.json")
 ref = json.loads(open(G + "bench_reference.json").read().strip().splitlines()[-1])
-out = ["# Round-1 bench matrix (1 B200, `python bench.py --workload W`), final round-1 kernels", "",
+out = [f"# {R} bench matrix (1 B200, `python bench.py --workload W`)", "",
        "Weak scaling, L2 flushed (256 MiB write) between timed steps; launches that each fill the GPU for >= 2 "
        "waves run back to back, others concurrently on separate streams; clocks 1965 MHz with no throttle "
        "reason on every line; `cpu` = the CPU oracle on the box's 16 host threads (bounded sample, "
-       "`cpu_baseline`). Raw JSON lines: `r1_bench_matrix.jsonl`; reference arm (the oracle, C2): "
-       "`r1_bench_reference.json` (%.2e request-steps/s)." % ref["value"], "",
+       "`cpu_baseline`). Raw JSON lines: `%s_bench_matrix.jsonl`; reference arm (the oracle, C2): "
+       "`%s_bench_reference.json` (%.2e request-steps/s)." % (R, R, ref["value"]), "",
        "| workload | value | unit | ms/step | e2e | roofline frac (alu, dominant launch alone) | dominant | "
        "per-launch ms | cpu oracle | GPU/CPU |", "|---|---|---|---|---|---|---|---|---|---|"]
 for d in lines:
@@ -30,7 +31,7 @@ for d in lines:
     out.append(f"| {name} | {d['value']:.3e} | {d['unit']} | {d['ms_per_step']:.1f} | {d['e2e']['value']:.3e} | "
                f"{d['roofline']['frac']:.4f} | {d['roofline'].get('kernel')} | {km} | {cpu:.2e} | "
                f"{(d['value'] / cpu if cpu else 0):.0f}x |")
-open("profiles/r1_bench_matrix.md", "w").write("\n".join(out) + "\n")
+open(f"profiles/{R}_bench_matrix.md", "w").write("\n".join(out) + "\n")
 # launch list
 rows = list(csv.reader(open(G + f"launches_{tag}.csv")))
 h, agg, n = None, collections.OrderedDict(), collections.Counter()
@@ -48,21 +49,21 @@ for r in rows:
     agg[k] = agg.get(k, 0) + v
     n[k] += 1
 tot = sum(agg.values())
-o = ["# ncu launch list of `python bench.py --steps 2 --warmup 3 --no-cpu-baseline` (C2), round 1 final kernels", "",
-     "(cold-cache, serialised under ncu: compare shares, not absolutes; `sim_kernel<P, TRACE, RING>`: 0 WAIT, "
-     "2 FCFS; RING=1 class-ring engine; each FCFS step also has its speculative-capacity fallback launch, "
-     "empty unless a replication overflowed)", "", "| share | total ms | launches | kernel |", "|---|---|---|---|"]
+o = [f"# ncu launch list of `python bench.py --steps 2 --warmup 3 --no-cpu-baseline` (C2), {R}", "",
+     "(cold-cache, serialised under ncu: compare shares, not absolutes; `sim_kernel<P, TRACE, RING, SEG>`: "
+     "0 WAIT, 1 NESTED, 2 FCFS; RING=1 class-ring engine, SEG=1 segment engine; each FCFS step also has its "
+     "speculative-capacity fallback launch, empty unless a replication overflowed)", "", "| share | total ms | launches | kernel |", "|---|---|---|---|"]
 for k, v in sorted(agg.items(), key=lambda x: -x[1]):
     o.append(f"| {100 * v / tot:.2f}% | {v:.3f} | {n[k]} | `{k[:90]}` |")
-open("profiles/r1_launches_bench.md", "w").write("\n".join(o) + "\n")
-shutil.copy(G + f"launches_{tag}.csv", "profiles/r1_launches_bench.csv")
+open(f"profiles/{R}_launches_bench.md", "w").write("\n".join(o) + "\n")
+shutil.copy(G + f"launches_{tag}.csv", f"profiles/{R}_launches_bench.csv")
 # ncu full summary + traffic
 subprocess.check_call([sys.executable, "tools/ncu_summary.py", G + f"prof_{tag}.ncu-rep", "/tmp/ncu_sum.md",
                        "/tmp/traffic.json"])
 txt = open("/tmp/ncu_sum.md").read().splitlines()
-txt[0] = (f"# ncu --set full summary, C2 bench launches (class-ring engine: sim_kernel<0,0,1> WAIT, "
-          f"sim_kernel<2,0,1> FCFS + its empty fallback launch), final round-1 kernels (`{G}prof_{tag}.ncu-rep`)")
-open("profiles/r1_ncu_full_c2.md", "w").write("\n".join(txt) + "\n")
+txt[0] = (f"# ncu --set full summary, C2 bench launches (class-ring engine: sim_kernel<0,0,1,0> WAIT, "
+          f"sim_kernel<2,0,1,0> FCFS + its empty fallback launch), {R} (`{G}prof_{tag}.ncu-rep`)")
+open(f"profiles/{R}_ncu_full_c2.md", "w").write("\n".join(txt) + "\n")
 t = json.load(open("profiles/traffic.json"))
 new = json.load(open("/tmp/traffic.json"))
 t["C2:wait"], t["C2:fcfs"] = new["wait"], new["fcfs"]
