@@ -171,12 +171,20 @@ int sched_thresholds(sched_t h, int32_t mode, double delta, double budget_B,
                      sched_threshold_report* out);
 
 /* Simulate global replications rep_begin .. rep_begin+n_reps-1 over [0, T)
- * with master seed `seed` (Philox stream layout DESIGN.md §4.2, so sharding
- * is invisible to the results).  Asynchronous on `cuda_stream`
- * (cudaStream_t, may be NULL); writes `out_dev`, a DEVICE uint64 array of
- * SCHED_NF * n_reps (field-major).  Needs thresholds (WAIT / NESTED).
- * Sync errors: SCHED_E_INVALID, SCHED_E_CUDA.  Capacity overflows are
- * reported per replication in SCHED_F_STATUS. */
+ * with master seed `seed`: independent Poisson arrival streams per prompt
+ * type (§Model; Philox stream layout DESIGN.md §4.2, so
+ * sharding is invisible to the results), scheduled by Algorithm 1 WAIT
+ * (PAPER.md:1457-1496), Algorithm 2 Nested WAIT or the
+ * FCFS baselines under the KV limit M with LIFO
+ * eviction (Eq. memory_constraint), batch time
+ * d0 + d1 tokens (Eq. time_consump) and the throughput /
+ * latency / TTFT accounting of PAPER.md:1235-1242.  Asynchronous on
+ * `cuda_stream` (cudaStream_t, may be NULL); writes `out_dev`, a DEVICE
+ * uint64 array of SCHED_NF * n_reps (field-major, caller-owned).  Needs
+ * thresholds (WAIT / NESTED).  Sync errors: SCHED_E_INVALID, SCHED_E_CUDA.
+ * Capacity overflows are reported per replication in SCHED_F_STATUS (1
+ * resident capacity, 2 restart pool) and in the handle's sticky status
+ * mask (sched_get_status). */
 int sched_run(sched_t h, uint64_t seed, uint64_t rep_begin, uint32_t n_reps,
               double horizon_s, uint64_t* out_dev, void* cuda_stream);
 
@@ -202,16 +210,24 @@ typedef struct {
   int32_t max_resident, restart_cap;      /* safe capacity, restart pool entries */
   int32_t spec_resident;                  /* main-launch capacity (== max_resident: no fallback) */
   int32_t fallback_grid, fallback_warps_per_block;
-  int32_t engine;                         /* 0 member engine (per-resident records, every
-                                             policy); 1 class-ring engine (WAIT / FCFS with
-                                             fixed per-class lengths; capacities
-                                             then count ring + staging records).  Chosen
-                                             automatically (ring unless its footprint exceeds
-                                             the member engine's by > 30%); the env var
-                                             WAITSIM_ENGINE=member|ring, read when the handle
-                                             is first launched, forces one. */
+  int32_t engine;                         /* 0 member engine (per-resident records: WAIT / FCFS
+                                             with length marks); 1 class-ring engine (WAIT /
+                                             FCFS with fixed per-class lengths; capacities
+                                             then count ring + staging records); 2 segment
+                                             engine (NESTED; spec_resident = its array,
+                                             fallback = the member engine's safe launch);
+                                             DESIGN.md §5.2.  The env var
+                                             WAITSIM_ENGINE=member|ring|seg, read when the
+                                             handle is first launched, forces one. */
 } sched_launch_info;
 int sched_get_launch_info(sched_t h, sched_launch_info* out);
+
+/* Sticky status of the handle (synchronous device read): bit s of *mask is
+ * set if some replication of a sched_run / sched_run_host / sched_run_trace
+ * since the previous call ended with status s != 0 (a replication re-run by
+ * the fallback launch reports the fallback's status only); the mask is then
+ * cleared.  Errors: SCHED_E_INVALID, SCHED_E_CUDA. */
+int sched_get_status(sched_t h, uint32_t* mask);
 
 /* Restart pool use (synchronous device read): capacity in entries and the
  * high-water mark (entries in chunks ever handed out; freed chunks are

@@ -31,8 +31,8 @@ F = {n: i for i, n in enumerate(FIELDS)}
 
 # every symbol include/sched.h declares
 EXPORTS = ["sched_create", "sched_thresholds", "sched_run", "sched_run_host",
-           "sched_run_trace", "sched_get_launch_info", "sched_restart_pool_stats", "sched_walks",
-           "sched_walks_host", "sched_destroy", "sched_last_error"]
+           "sched_run_trace", "sched_get_launch_info", "sched_get_status", "sched_restart_pool_stats",
+           "sched_walks", "sched_walks_host", "sched_destroy", "sched_last_error"]
 WALK_FIELDS = ["W_B", "stuck", "sumW", "maxW", "Wt_B", "viol", "sumX", "maxS", "minS", "S_B"]
 WF = {n: i for i, n in enumerate(WALK_FIELDS)}
 
@@ -105,6 +105,7 @@ def lib() -> C.CDLL:
                                       C.c_int64, C.POINTER(C.c_int64)]
         L.sched_get_launch_info.argtypes = [C.c_void_p, C.POINTER(LaunchInfo)]
         L.sched_restart_pool_stats.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.sched_get_status.argtypes = [C.c_void_p, C.POINTER(C.c_uint32)]
         L.sched_destroy.argtypes = [C.c_void_p]
         L.sched_walks.argtypes = [C.c_int32, C.c_int64, C.c_double, C.c_int64, C.c_double,
                                   C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p,
@@ -114,7 +115,7 @@ def lib() -> C.CDLL:
                                        C.c_int32]
         for name in ["sched_create", "sched_thresholds", "sched_run", "sched_run_host",
                      "sched_run_trace", "sched_get_launch_info", "sched_restart_pool_stats",
-                     "sched_walks", "sched_walks_host"]:
+                     "sched_get_status", "sched_walks", "sched_walks_host"]:
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -227,6 +228,13 @@ class Scheduler:
         li = LaunchInfo()
         _check(lib().sched_get_launch_info(self._h, C.byref(li)))
         return {n: getattr(li, n) for n, _ in LaunchInfo._fields_}
+
+    def status_mask(self) -> int:
+        """Sticky status (bit s: a replication ended with status s since the
+        previous call; cleared by the call)."""
+        m = C.c_uint32(0)
+        _check(lib().sched_get_status(self._h, C.byref(m)))
+        return m.value
 
     def restart_pool(self) -> dict:
         """Restart pool capacity and high-water mark, in entries (20 B each)."""

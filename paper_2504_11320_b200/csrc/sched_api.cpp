@@ -81,6 +81,7 @@ struct sched_s {
   unsigned long long* d_pool_free = nullptr;  // [0] free-stack head, [1] bump counter (low word)
   uint32_t pool_chunks = 0;
   uint32_t* d_counter = nullptr;
+  uint32_t* d_status = nullptr;              // sticky status mask (sched_get_status)
   uint64_t* d_out = nullptr;
   size_t out_cap = 0;
   // launch: main (speculative capacity) and fallback (safe capacity) per engine
@@ -309,6 +310,7 @@ int prepare(sched_s* h) {
       rec_safe += L.spare;
     }
     L.fallback = rec < rec_safe;
+    for (int c = 0; L.ring && c < K; ++c) L.fallback = L.fallback || L.rcap[c] < L.rcap_safe[c];
     int wpb = 1, bps = 0;
     if (int rc = size_launch(L.ring, rec, &L.warp_smem, &wpb, &bps)) return rc;
     L.wpb = wpb;
@@ -403,7 +405,7 @@ int prepare(sched_s* h) {
       if (warps * stride > h->ring_g_cap) {
         cudaFree(h->d_ring_g);
         h->d_ring_g = nullptr;
-        CK(cudaMalloc(&h->d_ring_g, warps * stride * 16));
+        CK(cudaMalloc(&h->d_ring_g, warps * stride * 16));  // {arrival | ft, clock} per record
         h->ring_g_cap = warps * stride;
       }
       if (warps > h->ring_log_warps) {
@@ -418,7 +420,30 @@ int prepare(sched_s* h) {
   // instead of a pass over every resident; replications
   // that overflow its array re-run on the member engine's safe launch
   h->use_seg = false;
-  if (h->in.policy == SCHED_NESTED && !(eng && std::string(eng) == "member")) {
+  // measured exceptions, where the member engine wins: a single segment
+  // (C1 Nested: nothing to skip, 84 vs 89 ms) and decode-length marks with
+  // M^pi > M (C5: thrashing LIFO eviction of mostly entry-stage residents,
+  // tombstones of mid-segment completions: 2.46 vs 2.89 s per 1,818 s)
+  bool seg_wins = true;
+  if (h->in.policy == SCHED_NESTED) {
+    bool marks = false;
+    double el = 0, lam = 0, mpi = 0;
+    for (size_t c = 0; c < h->in.lambda.size(); ++c) {
+      marks = marks || h->in.lp[c].size() > 1;
+      double w = 0, e = 0;
+      for (auto& t : h->in.l[c]) { w += (double)t.second; e += (double)t.second * t.first; }
+      if (w > 0) { el += h->in.lambda[c] * e / w; lam += h->in.lambda[c]; }
+    }
+    el = lam > 0 ? el / lam : 1.0;
+    uint32_t prev = 0;
+    for (size_t k = 0; k < h->in.seg_end.size() && k < h->in.thresholds.size(); ++k) {
+      for (uint32_t st = (k ? prev + 1 : 0); st <= h->in.seg_end[k]; ++st) mpi += h->in.thresholds[k] * (el + st);
+      prev = h->in.seg_end[k];
+    }
+    seg_wins = h->in.seg_end.size() > 1 && !(marks && mpi > (double)h->in.M);
+  }
+  const bool seg_forced = eng && std::string(eng) == "seg";
+  if (h->in.policy == SCHED_NESTED && !(eng && std::string(eng) == "member") && (seg_wins || seg_forced)) {
     LaunchCfg& L = h->sg;
     L = LaunchCfg{};
     L.seg = true;
@@ -436,7 +461,7 @@ int prepare(sched_s* h) {
       L.grid = h->sm_count * bps;
       L.fallback = true;  // the member engine's safe launch
       h->use_seg = true;
-    } else if (eng && std::string(eng) == "seg") {
+    } else if (seg_forced) {
       return SCHED_E_INVALID;
     }
     if (h->use_seg) {
@@ -466,6 +491,10 @@ int prepare(sched_s* h) {
     CK(cudaMemcpy(h->d_pool_free, init, 16, cudaMemcpyHostToDevice));
   }
   if (!h->d_counter) CK(cudaMalloc(&h->d_counter, 16));  // [main, fallback, retry count]
+  if (!h->d_status) {
+    CK(cudaMalloc(&h->d_status, 4));
+    CK(cudaMemset(h->d_status, 0, 4));
+  }
   DevParams& p = h->base;
   p.n_rings = n_rings;
   for (size_t i = 0; i < h->in.thresholds.size() && i < 32; ++i) p.thr[i] = h->in.thresholds[i];
@@ -479,6 +508,7 @@ int prepare(sched_s* h) {
   p.pool_bump = (uint32_t*)(h->d_pool_free + 1);
   p.pool_chunks = h->pool_chunks;
   p.work_counter = h->d_counter;
+  p.status_mask = h->d_status;
   {
     // per-slot restart-chunk stashes: slots of the widest launch of any engine
     uint64_t slots = 1;
@@ -496,6 +526,13 @@ int prepare(sched_s* h) {
       h->stash_words = words;
     }
     p.pool_stash = h->d_pool_stash;
+    // stashes hold at most half of the pool, so a small pool is not
+    // exhausted by chunks parked in idle stashes (a stash below ~11 chunks
+    // sends eviction-heavy FIFOs back to the contended free stack: C4
+    // rho=0.95 WAIT 8.4 ms with 11, 60 ms with 7)
+    const uint64_t share = (uint64_t)h->pool_chunks / (2 * slots * (uint64_t)n_rings);
+    p.stash_lim = (uint32_t)std::min<uint64_t>(11, share);
+    p.bump_n = std::min<uint32_t>(4, p.stash_lim + 1);
   }
   p.ring_g = h->d_ring_g;
   p.ring_log = h->d_ring_log;
@@ -513,7 +550,7 @@ void set_caps(DevParams& p, const LaunchCfg& L, bool safe, int K) {
   p.warp_smem = safe ? L.fb_warp_smem : L.warp_smem;
   uint32_t off = 0;
   for (int c = 0; c < K; ++c) {
-    p.rcap[c] = L.ring ? L.rcap_safe[c] : 0u;
+    p.rcap[c] = L.ring ? (safe ? L.rcap_safe[c] : L.rcap[c]) : 0u;
     p.roff[c] = off;
     off += p.rcap[c];
   }
@@ -939,6 +976,17 @@ int sched_get_launch_info(sched_t h, sched_launch_info* out) {
   return SCHED_OK;
 }
 
+int sched_get_status(sched_t h, uint32_t* mask) {
+  if (!h || !mask) return fail(SCHED_E_INVALID, "null argument");
+  *mask = 0;
+  if (!h->d_status) return SCHED_OK;  // never launched
+  CK(cudaSetDevice(h->device));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(mask, h->d_status, 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemset(h->d_status, 0, 4));
+  return SCHED_OK;
+}
+
 int sched_restart_pool_stats(sched_t h, uint64_t* capacity_entries, uint64_t* high_water_entries) {
   if (!h || !capacity_entries || !high_water_entries) return fail(SCHED_E_INVALID, "null argument");
   *capacity_entries = (uint64_t)h->pool_chunks * kRestartChunk;
@@ -1015,6 +1063,7 @@ void sched_destroy(sched_t h) {
   cudaFree(h->d_pool_next);
   cudaFree(h->d_pool_free);
   cudaFree(h->d_counter);
+  cudaFree(h->d_status);
   cudaFree(h->d_out);
   cudaFree(h->d_retry);
   cudaFree(h->d_rf_B);

@@ -89,7 +89,10 @@ struct DevParams {
   uint32_t* pool_bump;     // chunks handed out so far (high-water mark)
   uint32_t pool_chunks;
   uint32_t* pool_stash;    // [warp slots][n_rings] x {count, 11 chunks}: per-slot free chunks (persist)
+  uint32_t stash_lim;      // chunks a stash may hold (<= 11; 0 for pools too small to share out)
+  uint32_t bump_n;         // never-used chunks taken per bump allocation (<= stash_lim + 1)
   uint32_t* work_counter;  // this launch's replication counter
+  uint32_t* status_mask;   // handle's sticky status: bit s = a replication ended with status s
   // speculative capacity: the main launch runs with a small resident
   // capacity; replications that overflow it are appended to retry_list and
   // re-run from scratch by a fallback launch with the safe capacity

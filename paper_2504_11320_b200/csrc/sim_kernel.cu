@@ -168,16 +168,6 @@ struct __align__(16) Rec {
   int64_t a;
   uint64_t q;
 };
-// class-ring engine resident: arrival tick, admission clock x (bits 0-29) |
-// first token pending at the next participation (bit 30, valid while
-// x = C - 1) | first token emitted or pending (bit 31), admission sequence
-// number (LIFO order)
-struct __align__(16) RRec {
-  int64_t a;
-  uint32_t xf;
-  uint32_t seq;
-};
-constexpr uint32_t XF_FT = 0x80000000u, XF_PEND = 0x40000000u, XF_X = 0x3FFFFFFFu;
 constexpr uint32_t kRingLog = 1u << 16;  // admission-log entries per warp (class-ring engine)
 // segment-engine resident (NESTED), shared memory: l | l' << 16,
 // cohort clock x (bits 0-30: the segment clock at which it ran its entry
@@ -315,7 +305,9 @@ struct WarpSim {
   const int lane;
   // shared-memory views (this warp's slice)
   Rec* rr;                           // [Rc] residents in admission order (RING: staged admissions)
-  RRec* rg;                          // RING: class rings in global memory (ring c: P.rcap[c] records from P.roff[c])
+  ulonglong2* rg;                    // RING: class rings in global memory (ring c: P.rcap[c] records from P.roff[c]):
+                                     //   {arrival tick | first token emitted before admission (restart) << 63,
+                                     //    admission clock x}: one 16-B store per admission
   uint32_t* coh;                     // RING: [ccsize] members admitted at class clock x, slot x mod (l'_c + 1)
   int64_t* vt;                       // [K][32] generated window (t): visibility + admission
   uint16_t* vl; uint16_t* vlp;       // [K][32] generated window (l, l')
@@ -393,7 +385,7 @@ struct WarpSim {
     // RING: spare staging slots hold the victims of one eviction round
     vt = (int64_t*)(rr + Rc);
     if (RING) {
-      rg = (RRec*)p.ring_g + (size_t)slot * p.ring_stride;
+      rg = (ulonglong2*)p.ring_g + (size_t)slot * p.ring_stride;
       coh = (uint32_t*)(rr + Rc + p.spare);
       vt = (int64_t*)((unsigned char*)coh + ((p.ccsize * 4u + 15u) & ~15u));
     }
@@ -473,10 +465,10 @@ struct WarpSim {
       if (prev == old) return (uint32_t)old;
       old = prev;
     }
-    const uint32_t c = atomicAdd(P.pool_bump, kBump);
+    const uint32_t c = atomicAdd(P.pool_bump, P.bump_n);
     if (c >= P.pool_chunks) return kNoChunk;
     // the rest of the batch goes to the stash (it is empty here)
-    const uint32_t extra = min(kBump, P.pool_chunks - c) - 1;
+    const uint32_t extra = min(P.bump_n, P.pool_chunks - c) - 1;
     for (uint32_t i = 0; i < extra; ++i) sq[5 + i] = c + 1 + i;
     sq[4] = extra;
     return c;
@@ -498,7 +490,7 @@ struct WarpSim {
   __device__ void pool_release_chain(int q, uint32_t first, uint32_t k) const {
     uint32_t* sq = rq + 16 * q;
     uint32_t n = sq[4];
-    while (k > 0 && n < kStash) {
+    while (k > 0 && n < P.stash_lim) {
       sq[5 + n++] = first;
       if (--k) first = __ldcg(P.pool_next + first);
     }
@@ -675,10 +667,9 @@ struct WarpSim {
         if (lane == 0) st->arrivals += n;
         if (lane == c) k_vis += n;
         if (j + n < 32) break;
-        maybe_flush();
+        maybe_flush();  // a long backlog: one more tick per lane per window
       }
     }
-    maybe_flush();
   }
 
   // next not-yet-visible arrival tick (< T), TMAX if none
@@ -974,18 +965,21 @@ struct WarpSim {
         }
         if (__all_sync(FULL, ok)) {
           const Seg sg{o1, len1, o2};
-          // every waiting arrival was offered (no class beyond 32): taking
-          // all of them ends the admissions
-          const bool capped = __any_sync(FULL, pend > 32u);
+          // each class offers its first min(pending, want, 32) arrivals: a
+          // candidate's rank is at least its index in its class, so ranks
+          // below `want` stay exact; when none was capped,
+          // taking every offered one ends the admissions
+          const uint32_t cap = min(want, 32u);
+          const bool capped = __any_sync(FULL, pend > cap);
           if (c_hi - c_lo == 1) {
-            const int r = take_single<FCFS_COND>(c_lo, min(pend, 32u), sg, want);
+            const int r = take_single<FCFS_COND>(c_lo, min(pend, cap), sg, want);
             if (r < 0) return false;
             if (r == 0 || (r == 2 && !capped)) break;
             continue;
           }
           // FCFS admits whole chunks: per-class ranking wins for K <= 4
           // (measured C2 FCFS +12%, C4 +8-10%); Nested takes n_1 <= few
-          const uint32_t pc = min(pend, 32u);
+          const uint32_t pc = min(pend, cap);
           const int r = !FCFS_COND ? take_merged<FCFS_COND>(pc, sg, want)
                       : P.K == 2 ? take_merged_k<FCFS_COND, 2>(pc, sg, want)
                       : P.K == 3 ? take_merged_k<FCFS_COND, 3>(pc, sg, want)
@@ -1359,10 +1353,13 @@ struct WarpSim {
       const uint32_t rn = __shfl_sync(FULL, r_n, (int)v), head = __shfl_sync(FULL, r_head, (int)v);
       const uint32_t Cv = __shfl_sync(FULL, r_C, (int)v), Rv = __shfl_sync(FULL, r_Ri, (int)v);
       const bool res = valid && j < rn;
-      RRec e = {0, 0, 0};
-      if (res) e = rg[P.roff[v] + wrap(head + (rn - 1 - j), P.rcap[v])];
-      const uint32_t xf = e.xf, x = xf & XF_X;
+      ulonglong2 rr2 = make_ulonglong2(0ull, (unsigned long long)Cv);
+      if (res) rr2 = __ldcg(rg + P.roff[v] + wrap(head + (rn - 1 - j), P.rcap[v]));
+      const uint64_t rec = rr2.x;
+      const uint32_t x = (uint32_t)rr2.y;  // admission clock
       const uint32_t fl = P.fl[v], l = fl & 0xFFFFu, lp = fl >> 16;
+      const int64_t e_a = (int64_t)(rec & 0x7FFFFFFFFFFFFFFFull);
+      const bool ft0 = (rec >> 63) != 0;  // first token emitted before this admission
       const uint32_t s = Cv - x;  // next stage to run
       const uint32_t inp = res && (POL == SCHED_WAIT ? ((Qmask >> v) & 1u) : 1u);
       const uint32_t f = res ? (l + s - 1 + inp) : 0u;
@@ -1372,7 +1369,7 @@ struct WarpSim {
       const bool ev = res && (uint32_t)lane < ntr;
       const uint32_t ne = __popc(__ballot_sync(FULL, ev));
       // a first token still pending (admitted at the last participation) was not emitted
-      const bool pend = ev && (xf & XF_PEND) && x == Cv - 1;
+      const bool pend = ev && !ft0 && x == Cv - 1;
       // restart records in eviction order (re-enter the queue)
       const int q = POL == SCHED_WAIT ? (int)v : 0;
       const uint32_t gq = __match_any_sync(FULL, ev ? (uint32_t)q : (0x100u + (uint32_t)lane));
@@ -1391,16 +1388,16 @@ struct WarpSim {
       __syncwarp();
       if (ev) {
         const size_t ri = fifo_wentry(q, tail_q + before);
-        P.pool_a[ri] = e.a;
+        P.pool_a[ri] = e_a;
         P.pool_e[ri] = now;
         // ring engine: lengths are the class's, so the record keeps the class
-        P.pool_llp[ri] = v | (((xf & XF_FT) && !pend) ? 0x80000000u : 0u);
+        P.pool_llp[ri] = v | (!pend ? 0x80000000u : 0u);
         sh_add_u32(&cnt[v], 1u);
         sh_add_u64(&xs[v], (uint64_t)x);
-        acc_ev += (uint64_t)e.a;
+        acc_ev += (uint64_t)e_a;
         // the victim leaves its cohort (stage s = C - x in 1..l')
         sh_add_u32(&coh[P.ccoff[v] + (Rv >= s ? Rv - s : Rv + lp + 1 - s)], ~0u);
-        if (pend) { sh_add_u32(&cnt[32 + v], ~0u); sh_add_u64(&psum()[v], (uint64_t)(-e.a)); }
+        if (pend) { sh_add_u32(&cnt[32 + v], ~0u); sh_add_u64(&psum()[v], (uint64_t)(-e_a)); }
       }
       __syncwarp();
       if (lane < K) {
@@ -2010,7 +2007,7 @@ struct WarpSim {
         for (uint32_t cm = __ballot_sync(FULL, my_nd > 0); cm; cm &= cm - 1) {
           const int c = __ffs(cm) - 1;
           const uint32_t n = bcast32(my_nd, c), head = bcast32(r_head, c), cap = P.rcap[c];
-          for (uint32_t j = lane; j < n; j += 32) al += (uint64_t)rg[P.roff[c] + wrap(head + j, cap)].a;
+          for (uint32_t j = lane; j < n; j += 32) al += __ldcg(&rg[P.roff[c] + wrap(head + j, cap)].x) & 0x7FFFFFFFFFFFFFFFull;
         }
         al = warp_sum_u128(al);
         if (lane == 0) st->acc_ev += al;
@@ -2050,7 +2047,8 @@ struct WarpSim {
       // a prompt without its first token emits it at the next participation
       const bool pend = v && !(meta & META_FT);
       if (v) {
-        rg[P.roff[c] + wrap(head + n + rk, cap)] = RRec{e.a, C | XF_FT | (pend ? XF_PEND : 0u), seq_next + j};
+        rg[P.roff[c] + wrap(head + n + rk, cap)] =
+            make_ulonglong2((uint64_t)e.a | (pend ? 0ull : 1ull << 63), (unsigned long long)C);
         P.ring_log[(size_t)wslot * kRingLog + ((seq_next + j) & (kRingLog - 1))] = (uint8_t)c;
         acc_adm += (uint64_t)e.a;
         if (rk == 0) cnt[c] = __popc(grp);
@@ -2080,7 +2078,7 @@ struct WarpSim {
     u128 ar = 0;
     for (int c = 0; c < P.K; ++c) {
       const uint32_t n = bcast32(r_n, c), head = bcast32(r_head, c), cap = P.rcap[c];
-      for (uint32_t j = lane; j < n; j += 32) ar += (uint64_t)rg[P.roff[c] + wrap(head + j, cap)].a;
+      for (uint32_t j = lane; j < n; j += 32) ar += __ldcg(&rg[P.roff[c] + wrap(head + j, cap)].x) & 0x7FFFFFFFFFFFFFFFull;
     }
     ar = warp_sum_u128(ar);
     if (lane == 0) st->acc_done_a = st->acc_adm - st->acc_ev - ar;
@@ -2360,8 +2358,11 @@ __global__ void __launch_bounds__((POL == SCHED_WAIT || RING) ? 128 : 256, (POL 
       break;
     }
     sim.run(r);
-    if (!P.fallback && P.retry_list && sim.status == 1 && lane == 0)
-      P.retry_list[atomicAdd(P.retry_count, 1u)] = r;  // re-run with the safe capacity
+    if (!P.fallback && P.retry_list && sim.status == 1) {
+      if (lane == 0) P.retry_list[atomicAdd(P.retry_count, 1u)] = r;  // re-run with the safe capacity
+    } else if (sim.status && lane == 0) {
+      atomicOr(P.status_mask, 1u << min(sim.status, 31u));
+    }
   }
   sim.flush_stash();
 }

@@ -254,8 +254,18 @@ def test_speculative_capacity_fallback(spec, engine, monkeypatch):
 
 
 def test_capacity_overflow_is_reported():
-    rows = gpu_rows(W.C2, W.Policy(W.FCFS, B=1024), [0], 4, horizon_s=1.0, max_resident=64)
+    """A safe capacity below the population: status 1 in every row and in the
+    handle's sticky status mask (sched_get_status), which a read clears."""
+    from paper_2504_11320_b200 import Scheduler
+    s = Scheduler(W.C2, W.Policy(W.FCFS, B=1024), max_resident=64)
+    assert s.status_mask() == 0
+    rows = s.run_host(W.C2.seed, 0, 4, 1.0)
     assert (rows[oracle.F["status"]] == 1).all()
+    assert s.status_mask() == 1 << 1
+    assert s.status_mask() == 0
+    s.run_host(W.C2.seed, 0, 4, 0.001)  # too short to overflow
+    assert s.status_mask() == 0
+    s.close()
 
 
 def test_full_size_bench_config_sampled():
@@ -392,13 +402,19 @@ def test_engine_selection_rule(monkeypatch):
     """the class-ring engine for every fixed-length WAIT /
     FCFS configuration (its member records live in global memory, so its
     footprint no longer depends on the population), the segment engine for
-    Nested, the member engine for length marks under WAIT / FCFS."""
+    Nested except one segment or decode-length marks with M^pi > M (member
+    engine, measured faster there), the member engine for length marks under
+    WAIT / FCFS."""
     from paper_2504_11320_b200 import Scheduler
     monkeypatch.delenv("WAITSIM_ENGINE", raising=False)
     eng = lambda wl, pol, thr=None: Scheduler(wl, pol, thr).launch_info()["engine"]
     assert eng(W.C2, W.Policy(W.WAIT), [16, 16]) == 1
     assert eng(W.C2, W.Policy(W.FCFS, B=1024)) == 1
     assert eng(W.C3A, W.Policy(W.NESTED, seg_end=SEG3A), [7, 7, 7, 5]) == 2
+    assert eng(W.C3B, W.Policy(W.NESTED, seg_end=SEG10), fl.nested_strict(W.C3B, SEG10)) == 2
+    assert eng(W.c4(4), W.Policy(W.NESTED, seg_end=SEG4), [46, 23, 8]) == 2
+    assert eng(W.C1, W.Policy(W.NESTED, seg_end=[16]), [1]) == 0          # one segment
+    assert eng(W.c5(55.0), W.Policy(W.NESTED, seg_end=SEG10), [11, 8, 6, 5, 4, 3, 2, 2, 2, 2]) == 0  # marks, M^pi > M
     monkeypatch.setenv("WAITSIM_ENGINE", "member")
     assert eng(W.C3A, W.Policy(W.NESTED, seg_end=SEG3A), [7, 7, 7, 5]) == 0
     assert eng(W.C2, W.Policy(W.FCFS, B=1024)) == 0
@@ -407,6 +423,121 @@ def test_engine_selection_rule(monkeypatch):
     assert eng(W.c4(1), W.Policy(W.FCFS, B=1024)) == 1               # long decodes
     assert eng(W.c4(4), W.Policy(W.WAIT), [18, 12, 6]) == 1
     assert eng(W.c4(2), W.Policy(W.WAIT), [6, 4, 2]) == 1
+
+
+@pytest.mark.parametrize("name", ["C3a", "C3b", "C4", "C5"])
+def test_full_size_bench_workloads_sampled(name):
+    """Every bench workload at its bench launch configuration (bench.py's
+    registry: replication counts, horizons, thresholds from sched_thresholds,
+    handle options), sampled replications checked against the oracle one by
+    one, conservation and the memory bound checked on every row."""
+    import importlib.util
+    import os
+    from paper_2504_11320_b200 import Scheduler
+    from paper_2504_11320_b200.sim import run_rows
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    pols, reps, _ = bench.expand(name)
+    if name == "C4":
+        pols = [p for p in pols if p[0].endswith("@0.5") or p[0].endswith("@0.9")]
+    kw = bench.SCHED_KW.get(name, {})
+    n_check = 2 if name == "C5" else 4
+    for label, pol, thr, wl in pols:
+        s = Scheduler(wl, pol, thr, **kw)
+        if thr is None and pol.kind in (W.WAIT, W.NESTED):
+            thr = s.thresholds()["thresholds"]
+        rows = run_rows(s, wl.seed, 0, reps, wl.horizon_s)
+        torch.cuda.synchronize()
+        got = rows.cpu().numpy().view(np.uint64)
+        s.close()
+        assert (got[oracle.F["status"]] == 0).all(), label
+        for i in np.linspace(0, reps - 1, n_check).astype(int).tolist():
+            ref = oracle.run(wl, pol, thr if thr is not None else [0], n_reps=1, rep_begin=i)
+            assert_rows_equal(got[:, i:i + 1], ref, f"{name}/{label} rep {i}")
+        f = lambda k: got[oracle.F[k]].astype(object)
+        assert (f("arrivals") == f("completed") + f("completed_after_T") + f("final_waiting")
+                + f("final_resident")).all()
+        assert (got[oracle.F["max_kv_peak"]] <= wl.M).all()
+
+
+def test_r28_trace_log():
+    """Reading R28 (class-major simultaneous WAIT admissions decide the LIFO
+    victim), the hand-traced CPU pin's trace through sched_run_trace."""
+    from paper_2504_11320_b200 import Scheduler
+    from test_oracle import _r28_trace
+    wl, tr = _r28_trace()
+    ref_rows, ref_log = oracle.run_trace(wl, W.Policy(W.WAIT), [1, 1], [tr], log_cap=8)
+    s = Scheduler(wl, W.Policy(W.WAIT), [1, 1])
+    rows, log = s.run_trace([tr], wl.horizon_s, log_cap=8)
+    assert np.array_equal(log, ref_log)
+    assert_rows_equal(rows, ref_rows, "R28")
+    assert (int(log[1][2]), int(log[1][4])) == (5, 1)  # tokens, evictions of batch 2
+
+
+# ---------------------------------------------- hand traces (tests/hand_traces.py)
+@pytest.mark.parametrize("case", ["nested_A", "nested_B", "fcfs_budget"])
+def test_hand_traces_replayed(case):
+    """The hand-derived batch logs and rows of the multi-segment Nested WAIT
+    traces (Alg. 2: k* prefix, >= at equality,
+    oldest-first entry stage, paused KV, LIFO cascade) and the FCFS token
+    budget, replayed through sched_run_trace: equal to the hand values and
+    to the oracle, element by element."""
+    import hand_traces as H
+    from paper_2504_11320_b200 import Scheduler
+    if case == "fcfs_budget":
+        wl, pol, thr, T, log_exp, row_exp = (H.fcfs_workload(), H.FCFS_POLICY, [0], 10.0, H.FCFS_LOG,
+                                             H.FCFS_ROW)
+        tr = H.FCFS_TRACE
+    else:
+        M, log_exp, row_exp = ((H.NESTED_A_M, H.NESTED_A_LOG, H.NESTED_A_ROW) if case == "nested_A"
+                               else (H.NESTED_B_M, H.NESTED_B_LOG, H.NESTED_B_ROW))
+        wl, pol, thr, T, tr = H.nested_workload(M), H.NESTED_POLICY, H.NESTED_THR, H.NESTED_T_S, H.NESTED_TRACE
+    s = Scheduler(wl, pol, thr if pol.kind != W.FCFS else None)
+    rows, log = s.run_trace([tr], T, log_cap=64)
+    s.close()
+    assert [tuple(int(x) for x in r) for r in log] == log_exp
+    assert H.row_matches(rows, 0, row_exp, oracle.F, oracle.u128) == {}
+    ref_rows, ref_log = oracle.run_trace(wl, pol, thr, [tr], log_cap=64, horizon_s=T)
+    assert np.array_equal(log, ref_log)
+    assert_rows_equal(rows, ref_rows, case)
+
+
+# ------------------------------------------------ restart pool (DESIGN.md §5.3)
+def test_restart_pool_chunks_are_reused():
+    """C1 WAIT evicts ~280 prompts per replication; 16,384 replications push
+    ~4.6M restart entries through a pool of 2^19 (8,192 chunks, more than
+    the ~4,700 warps in flight each hold while a restart waits): chunks are
+    returned and reused, every row has status 0, sampled rows equal the
+    oracle and the high-water mark stays within the pool."""
+    from paper_2504_11320_b200 import Scheduler
+    s = Scheduler(W.C1, W.Policy(W.WAIT), [1], restart_cap=1 << 19)
+    rows = s.run_host(W.C1.seed, 0, 16384, W.C1.horizon_s)
+    pool = s.restart_pool()
+    s.close()
+    assert (rows[oracle.F["status"]] == 0).all()
+    assert int(rows[oracle.F["evictions"]].astype(np.int64).sum()) > 4 * pool["capacity_entries"]
+    assert 0 < pool["high_water_entries"] <= pool["capacity_entries"]
+    for i in [0, 1, 5000, 16383]:
+        ref = oracle.run(W.C1, W.Policy(W.WAIT), [1], n_reps=1, rep_begin=i)
+        assert_rows_equal(rows[:, i:i + 1], ref, f"C1 rep {i}")
+
+
+def test_restart_pool_exhaustion_is_reported():
+    """A pool of one chunk cannot hold the concurrent restarts of 256 C1
+    replications: some rows report status 2, the others stay bit-exact."""
+    from paper_2504_11320_b200 import Scheduler
+    s = Scheduler(W.C1, W.Policy(W.WAIT), [1], restart_cap=64)
+    rows = s.run_host(W.C1.seed, 0, 256, W.C1.horizon_s)
+    assert s.status_mask() == 1 << 2
+    s.close()
+    st = rows[oracle.F["status"]]
+    assert (st == 2).any() and set(st.tolist()) <= {0, 2}
+    ok = np.nonzero(st == 0)[0][:4].tolist()
+    for i in ok:
+        ref = oracle.run(W.C1, W.Policy(W.WAIT), [1], n_reps=1, rep_begin=i)
+        assert_rows_equal(rows[:, i:i + 1], ref, f"C1 rep {i}")
 
 
 # ------------------------------- Nested: segment engine vs member engine

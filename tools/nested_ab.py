@@ -11,7 +11,8 @@ from paper_2504_11320_b200 import Scheduler
 from paper_2504_11320_b200.sim import run_rows
 
 SEG10 = [50 * k for k in range(1, 11)]
-WLS = [("C3a", W.C3A, [20, 40, 80, 160], None, 10000, None, {}),
+WLS = [("C1", W.C1, [16], [1], 16384, None, {}),
+       ("C3a", W.C3A, [20, 40, 80, 160], None, 10000, None, {}),
        ("C3a_tv", W.c3a_time_varying(), [20, 40, 80, 160], [11, 11, 10, 7], 10000, None, {}),
        ("C3b", W.C3B, SEG10, None, 10000, None, {})]
 WLS += [(f"C4_{i}", W.c4(i), [100, 200, 300], None, 2000, None, {}) for i in range(5)]
