@@ -125,7 +125,8 @@ inline uint32_t warp_smem_bytes(uint32_t Rc, int K, bool tv = false, bool ring =
   if (nested) b += ((Rc + 31u) / 32u + 15u) & ~15u;  // per-chunk activity summaries
   if (tv) b += (uint32_t)K * (32u * 16u);   // operational-time windows (generated, private)
   b = (b + 15u) & ~15u;
-  b += n_rings * 64u;                        // restart FIFO chunk cursors (head, head index, tail, tail index) + chunk stash
+  b += n_rings * 80u;                        // restart FIFO chunk cursors (head, head index, tail, tail index),
+                                            // chunk stash (count + 11), successors of head and tail
   return b;
 }
 

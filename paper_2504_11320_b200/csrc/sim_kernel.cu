@@ -417,13 +417,13 @@ struct WarpSim {
     vtau = (int64_t*)((unsigned char*)st + ((RING || SEG) ? 512 : 256) +
                       (POL == SCHED_NESTED ? (((p.Rc + 31) / 32 + 15) & ~15u) : 0u));
     atau = vtau + p.K * 32;
-    rq = (uint32_t*)(base + p.warp_smem - p.n_rings * 64u);
+    rq = (uint32_t*)(base + p.warp_smem - p.n_rings * 80u);
     if (lane < p.n_rings) {  // this slot's chunk stash, kept in global memory between launches
       const uint4* g = reinterpret_cast<const uint4*>(p.pool_stash) + ((size_t)slot * p.n_rings + lane) * 3;
       for (int i = 0; i < 3; ++i) {  // count + kStash chunks = 12 words
         const uint4 sv = g[i];
-        rq[16 * lane + 4 + 4 * i] = sv.x; rq[16 * lane + 5 + 4 * i] = sv.y;
-        rq[16 * lane + 6 + 4 * i] = sv.z; rq[16 * lane + 7 + 4 * i] = sv.w;
+        rq[20 * lane + 4 + 4 * i] = sv.x; rq[20 * lane + 5 + 4 * i] = sv.y;
+        rq[20 * lane + 6 + 4 * i] = sv.z; rq[20 * lane + 7 + 4 * i] = sv.w;
       }
     }
   }
@@ -442,19 +442,21 @@ struct WarpSim {
 
   // ------------------------------------------- restart FIFOs (chunk pool)
   // FIFO q holds positions [rhead, rtail) (lane q's counters) in a linked
-  // list of kRestartChunk-entry chunks: rq[16q] = chunk of position rhead
-  // (index rq[16q+1] = its position / kRestartChunk), rq[16q+2] = chunk of
-  // the next write position rtail (index rq[16q+3]).  Free chunks come from
-  // a per-FIFO stash (rq[16q+4] = count, rq[16q+5..] = chunks; one per warp
+  // list of kRestartChunk-entry chunks: rq[20q] = chunk of position rhead
+  // (index rq[20q+1] = its position / kRestartChunk), rq[20q+2] = chunk of
+  // the next write position rtail (index rq[20q+3]), rq[20q+16] / [20q+17] =
+  // the successors of the head chunk and of the tail chunk (cached: a FIFO
+  // spanning two chunks needs no link read).  Free chunks come from
+  // a per-FIFO stash (rq[20q+4] = count, rq[20q+5..15] = chunks; one per warp
   // slot, kept in global memory between launches), else the device-wide
   // pool: a lock-free free stack of chunk chains (ABA tag in the high word),
   // else never-used chunks (handed out kBump at a time).  Passed and
   // released chunks go back to the stash, the overflow as ONE chain per
   // release (they are linked already): the free-stack head is one hot word,
   // so eviction-heavy runs (C4 rho >= 0.8, C5) must touch it rarely.
-  static constexpr uint32_t kStash = 11, kBump = 4;  // count + kStash = 12 words (3 x uint4)
+  static constexpr uint32_t kStash = 11, kBump = 4;  // count + kStash = 12 saved words (3 x uint4)
   __device__ uint32_t pool_alloc(int q) const {
-    uint32_t* sq = rq + 16 * q;
+    uint32_t* sq = rq + 20 * q;
     const uint32_t n = sq[4];
     if (n) { sq[4] = n - 1; return sq[4 + n]; }
     unsigned long long old = atomicAdd(P.pool_free, 0ull);
@@ -488,7 +490,7 @@ struct WarpSim {
   // return the k linked chunks first -> ... (k >= 1) of FIFO q: to the stash
   // while it has room, the rest as one chain
   __device__ void pool_release_chain(int q, uint32_t first, uint32_t k) const {
-    uint32_t* sq = rq + 16 * q;
+    uint32_t* sq = rq + 20 * q;
     uint32_t n = sq[4];
     while (k > 0 && n < P.stash_lim) {
       sq[5 + n++] = first;
@@ -502,63 +504,73 @@ struct WarpSim {
   }
   // pool entry of position pos (>= the committed head) of FIFO q
   __device__ __forceinline__ size_t fifo_entry(int q, uint32_t pos) const {
-    uint32_t c = rq[16 * q], ci = rq[16 * q + 1];
-    for (const uint32_t want = pos / kRestartChunk; ci < want; ++ci) c = __ldcg(P.pool_next + c);
+    const uint32_t want = pos / kRestartChunk, hi = rq[20 * q + 1];
+    uint32_t c = rq[20 * q];
+    if (want > hi) {  // the chunk after the head is cached (rq[20q+16]); further ones are walked
+      c = rq[20 * q + 16];
+      for (uint32_t ci = hi + 1; ci < want; ++ci) c = __ldcg(P.pool_next + c);
+    }
     return (size_t)c * kRestartChunk + pos % kRestartChunk;
   }
   // pool entry of tail position pos (the tail chunk or the one after it)
   __device__ __forceinline__ size_t fifo_wentry(int q, uint32_t pos) const {
-    uint32_t c = rq[16 * q + 2];
-    if (pos / kRestartChunk != rq[16 * q + 3]) c = __ldcg(P.pool_next + c);
+    uint32_t c = rq[20 * q + 2];
+    if (pos / kRestartChunk != rq[20 * q + 3]) c = rq[20 * q + 17];  // reserved successor of the tail
     return (size_t)c * kRestartChunk + pos % kRestartChunk;
   }
   // lane q: chunks for cnt (<= 32) more entries at the tail t of FIFO q
   // (the chunk of the next write position included); false: pool exhausted
   __device__ bool fifo_reserve(int q, uint32_t t, uint32_t cnt) const {
-    if (rq[16 * q + 2] == kNoChunk) {
+    if (rq[20 * q + 2] == kNoChunk) {
       const uint32_t c = pool_alloc(q);
       if (c == kNoChunk) return false;
-      rq[16 * q] = rq[16 * q + 2] = c;
-      rq[16 * q + 1] = rq[16 * q + 3] = t / kRestartChunk;
+      rq[20 * q] = rq[20 * q + 2] = c;
+      rq[20 * q + 1] = rq[20 * q + 3] = t / kRestartChunk;
+      rq[20 * q + 16] = rq[20 * q + 17] = kNoChunk;
     }
-    if ((t + cnt) / kRestartChunk > rq[16 * q + 3]) {
+    if ((t + cnt) / kRestartChunk > rq[20 * q + 3]) {
       const uint32_t c = pool_alloc(q);
       if (c == kNoChunk) return false;
-      __stcg(P.pool_next + rq[16 * q + 2], c);
+      __stcg(P.pool_next + rq[20 * q + 2], c);
+      rq[20 * q + 17] = c;
+      if (rq[20 * q + 2] == rq[20 * q]) rq[20 * q + 16] = c;  // the head's successor
     }
     return true;
   }
   // lane q, after the writes: the tail chunk follows the new tail position
   __device__ void fifo_tail_done(int q, uint32_t t_new) const {
-    if (t_new / kRestartChunk > rq[16 * q + 3]) {
-      rq[16 * q + 2] = __ldcg(P.pool_next + rq[16 * q + 2]);
-      rq[16 * q + 3] += 1;
+    if (t_new / kRestartChunk > rq[20 * q + 3]) {
+      rq[20 * q + 2] = rq[20 * q + 17];
+      rq[20 * q + 3] += 1;
+      rq[20 * q + 17] = kNoChunk;
     }
   }
   // lane q: return the chunks the committed head has passed
   __device__ void fifo_commit(int q, uint32_t head) const {
-    if (rq[16 * q + 2] == kNoChunk || rq[16 * q + 1] >= head / kRestartChunk) return;
-    const uint32_t first = rq[16 * q], k = head / kRestartChunk - rq[16 * q + 1];
-    uint32_t c = first;
-    for (uint32_t i = 0; i < k; ++i) c = __ldcg(P.pool_next + c);
-    rq[16 * q] = c;
-    rq[16 * q + 1] += k;
+    if (rq[20 * q + 2] == kNoChunk || rq[20 * q + 1] >= head / kRestartChunk) return;
+    const uint32_t first = rq[20 * q], k = head / kRestartChunk - rq[20 * q + 1];
+    uint32_t c = rq[20 * q + 16];  // the head's successor
+    for (uint32_t i = 1; i < k; ++i) c = __ldcg(P.pool_next + c);
+    rq[20 * q] = c;
+    rq[20 * q + 1] += k;
+    // successor of the new head: the tail's reserved successor, or a link
+    rq[20 * q + 16] = c == rq[20 * q + 2] ? rq[20 * q + 17] : __ldcg(P.pool_next + c);
     pool_release_chain(q, first, k);
   }
   // lanes < n_rings: save the chunk stash of this slot (kernel exit)
   __device__ void flush_stash() const {
     if (lane < P.n_rings) {
       uint4* g = reinterpret_cast<uint4*>(P.pool_stash) + ((size_t)wslot * P.n_rings + lane) * 3;
-      const uint32_t* sq = rq + 16 * lane;
+      const uint32_t* sq = rq + 20 * lane;
       for (int i = 0; i < 3; ++i) g[i] = make_uint4(sq[4 + 4 * i], sq[5 + 4 * i], sq[6 + 4 * i], sq[7 + 4 * i]);
     }
   }
   // lane q: return every chunk of FIFO q (end of the replication)
   __device__ void fifo_release_all(int q) const {
-    if (rq[16 * q + 2] == kNoChunk) return;
-    const uint32_t k = rq[16 * q + 3] - rq[16 * q + 1] + 1;  // head chunk .. tail chunk
-    pool_release_chain(q, rq[16 * q], k);
-    rq[16 * q] = rq[16 * q + 2] = kNoChunk;
+    if (rq[20 * q + 2] == kNoChunk) return;
+    const uint32_t k = rq[20 * q + 3] - rq[20 * q + 1] + 1;  // head chunk .. tail chunk
+    pool_release_chain(q, rq[20 * q], k);
+    rq[20 * q] = rq[20 * q + 2] = kNoChunk;
   }
   // NESTED stage info: segment index (bits 0-5), last stage of the segment
   // (bit 6), entry stage (bit 7); counter slot = segment (+32 at entry)
@@ -2227,7 +2239,7 @@ struct WarpSim {
     }
     __syncwarp();
     k_vis = vbase = k_adm = abase = pcount = rhead = rtail = 0;
-    if (lane < P.n_rings) rq[16 * lane] = rq[16 * lane + 2] = kNoChunk;
+    if (lane < P.n_rings) rq[20 * lane] = rq[20 * lane + 2] = kNoChunk;
     vprev = aprev = 0;
     newc = 0;
     r_head = r_n = r_C = seq_next = 0;
