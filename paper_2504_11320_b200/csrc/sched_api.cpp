@@ -541,6 +541,11 @@ int prepare(sched_s* h) {
   return 0;
 }
 
+void set_offsets(DevParams& p) {
+  p.off_csum = layout_off_csum(p.K, p.tv_any != 0);
+  p.off_rr = layout_off_rr(p.Rc, p.K, p.tv_any != 0, p.policy == SCHED_NESTED);
+}
+
 // capacities of one launch of configuration L (safe = the fallback launch)
 void set_caps(DevParams& p, const LaunchCfg& L, bool safe, int K) {
   p.ring_engine = L.ring ? 1u : 0u;
@@ -554,6 +559,7 @@ void set_caps(DevParams& p, const LaunchCfg& L, bool safe, int K) {
     p.roff[c] = off;
     off += p.rcap[c];
   }
+  set_offsets(p);
 }
 
 int launch(sched_s* h, DevParams p, cudaStream_t st, const LaunchCfg& L) {
@@ -579,6 +585,7 @@ int launch(sched_s* h, DevParams p, cudaStream_t st, const LaunchCfg& L) {
     q.seg_a = h->d_seg_a;
     q.Rc = L.Rc;
     q.warp_smem = L.warp_smem;
+    set_offsets(q);
     int grid = L.grid;
     if ((int64_t)p.n_reps < (int64_t)grid * L.wpb) grid = std::max<int>(1, (int)((p.n_reps + L.wpb - 1) / L.wpb));
     CK(launch_sim(q, grid, L.block, (size_t)L.wpb * L.warp_smem, st));

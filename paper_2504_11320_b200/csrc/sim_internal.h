@@ -56,6 +56,7 @@ struct DevParams {
   uint32_t hsize, csize;           // total buckets / cohort slots
   int64_t* seg_a;                  // [warps of the launch][seg_cap] arrival ticks of the residents (device)
   uint32_t warp_smem;      // bytes of shared memory per warp
+  uint32_t off_csum, off_rr;       // layout offsets that depend on Rc / tv (warp_smem_bytes)
   uint64_t seed;
   uint64_t rep_begin;      // global index of local replication 0
   uint32_t n_reps;
@@ -106,28 +107,30 @@ struct DevParams {
   int64_t* log_n;
 };
 
-// shared-memory bytes per warp for a given resident capacity / class count
+// Shared-memory layout of one warp (byte offsets; the kernel's WarpSim
+// constructor lays it out in this order): per class a generated and a
+// private admission window (32 x (t, l, l') each), 32 staged restart ticks,
+// counters / rank cursors / snapshot, WarpStats, eviction scratch -- all
+// offsets that depend on the class count only (immediates in the kernels
+// specialised on K) -- then the operational-time windows (time-varying
+// rates), Nested chunk summaries, residents / staged admissions (Rc x 16 B),
+// class-ring cohort counts or the segment engine's array, histograms and
+// cohort rings, and the restart-FIFO cursors + chunk stash at the end.
+inline uint32_t a16(uint32_t x) { return (x + 15u) & ~15u; }
+inline uint32_t layout_off_csum(int K, bool tv) {
+  return 768u * (uint32_t)K + 1280u + (tv ? 512u * (uint32_t)K : 0u);
+}
+inline uint32_t layout_off_rr(uint32_t Rc, int K, bool tv, bool nested) {
+  return layout_off_csum(K, tv) + (nested ? a16((Rc + 31u) / 32u) : 0u);
+}
 inline uint32_t warp_smem_bytes(uint32_t Rc, int K, bool tv = false, bool ring = false, bool nested = false,
                                 uint32_t n_rings = 1, uint32_t seg_cap = 0, uint32_t hsize = 0,
                                 uint32_t csize = 0, uint32_t extra = 0) {
-  uint32_t b = Rc * 16u;                    // residents: a (i64) + packed (l, l', s, meta)
-  b += (extra + 15u) & ~15u;                // class-ring engine: cohort counts per class clock slot
-  // segment engine: staging (Rc) + resident array (8 B records; arrival
-  // ticks in global memory) + histograms (3 x u32 per bucket) + cohort rings
-  // (2 x u32 per slot) + eviction scratch
-  if (seg_cap) b += seg_cap * 8u + ((hsize * 12u + csize * 8u + 15u) & ~15u) + 256u;
-  b += (uint32_t)K * (32u * 12u);           // generated windows (t, l, l')
-  b += (uint32_t)K * (32u * 12u);           // private admission windows (t, l, l')
-  b += 32u * 8u;                            // staged restart ticks
-  b += (64u + 32u + 32u) * 4u + 16u;        // counters, rank cursors, snapshot, align
-  b += 256u;                                // WarpStats (metric accumulators)
-  if (ring) b += 256u;                      // class-ring eviction scratch
-  if (nested) b += ((Rc + 31u) / 32u + 15u) & ~15u;  // per-chunk activity summaries
-  if (tv) b += (uint32_t)K * (32u * 16u);   // operational-time windows (generated, private)
-  b = (b + 15u) & ~15u;
-  b += n_rings * 80u;                        // restart FIFO chunk cursors (head, head index, tail, tail index),
-                                            // chunk stash (count + 11), successors of head and tail
-  return b;
+  uint32_t b = layout_off_rr(Rc, K, tv, nested) + Rc * 16u;
+  if (ring) b += a16(extra);                                    // cohort counts
+  if (seg_cap) b += seg_cap * 8u + a16(hsize * 12u + csize * 8u);  // segment engine
+  return b + n_rings * 80u;  // restart FIFO cursors (head, head index, tail, tail index),
+                             // chunk stash (count + 11), successors of head and tail
 }
 
 cudaError_t launch_sim(const DevParams& p, int grid, int block, size_t smem, cudaStream_t s);
