@@ -384,8 +384,10 @@ def bench_walks(args):
                          mu=c.get("mu", 0.0), n_prev=c.get("n_prev", 0), p=c.get("p", 0.0),
                          stream_ptr=stream.cuda_stream)
 
+    # warm-up walks use indices after the timed ones (K..K+W-1): walk_begin
+    # = (k * world + rank) * N stays small at any world size
     for k in range(args.warmup):
-        step(1000 + k)
+        step(args.steps + k)
     torch.cuda.synchronize()
     D.barrier()
     clocks = ClockSampler(local)
