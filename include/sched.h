@@ -219,6 +219,12 @@ typedef struct {
                                              DESIGN.md §5.2.  The env var
                                              WAITSIM_ENGINE=member|ring|seg, read when the
                                              handle is first launched, forces one. */
+  int32_t last_retries;                   /* replications of the handle's most recent
+                                             sched_run / sched_run_host that overflowed the
+                                             speculative capacity and re-ran in the fallback
+                                             launch (synchronous device read; 0 before the
+                                             first run).  Rows are unaffected (bit-exact);
+                                             this is a cost diagnostic. */
 } sched_launch_info;
 int sched_get_launch_info(sched_t h, sched_launch_info* out);
 

@@ -79,7 +79,7 @@ class LaunchInfo(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("grid", "block", "warps_per_block", "shared_bytes",
                                           "blocks_per_sm", "sm_count", "max_resident",
                                           "restart_cap", "spec_resident", "fallback_grid",
-                                          "fallback_warps_per_block", "engine")]
+                                          "fallback_warps_per_block", "engine", "last_retries")]
 
 
 _lib = None

@@ -378,7 +378,10 @@ int prepare(sched_s* h) {
       double adm = 0;
       for (int c = 0; c < K; ++c) {
         const double share = h->n_star_c[c] / h->n_star_total;
-        L.rcap[c] = std::min<uint32_t>(L.rcap_safe[c], (uint32_t)(1.2 * tot * share) + 48);
+        // class rings live in global memory (no occupancy cost): under
+        // time-varying rates the stationary estimate misses the peak-piece
+        // backlog (every C3a_tv replication overflowed it), so they stay safe
+        if (h->tv_peak <= 1.0) L.rcap[c] = std::min<uint32_t>(L.rcap_safe[c], (uint32_t)(1.2 * tot * share) + 48);
         adm += h->tv_peak * h->n_star_c[c] / (double)(in.lp[c][0].first + 1);
       }
       // admissions per batch ~ Poisson(adm): mean + 8 sd + 16 (tail < 1e-12)
@@ -980,6 +983,14 @@ int sched_get_launch_info(sched_t h, sched_launch_info* out) {
   out->fallback_grid = L.seg ? (h->mem.fallback ? h->mem.fb_grid : h->mem.grid) : L.fallback ? L.fb_grid : 0;
   out->fallback_warps_per_block = L.seg ? (h->mem.fallback ? h->mem.fb_wpb : h->mem.wpb) : L.fallback ? L.fb_wpb : 0;
   out->engine = L.seg ? 2 : L.ring ? 1 : 0;
+  out->last_retries = 0;
+  if (h->d_counter) {  // d_counter[2] = retry count of the last launch
+    uint32_t r = 0;
+    CK(cudaSetDevice(h->device));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(&r, h->d_counter + 2, 4, cudaMemcpyDeviceToHost));
+    out->last_retries = (int32_t)r;
+  }
   return SCHED_OK;
 }
 

@@ -595,3 +595,32 @@ def test_nested_engines_bit_exact(engine, case, monkeypatch):
     f = lambda k: got[oracle.F[k]].astype(object)
     assert (f("arrivals") == f("completed") + f("completed_after_T") + f("final_waiting")
             + f("final_resident")).all()
+
+
+@pytest.mark.parametrize("name", ["C2", "C3a", "C3a_tv", "C3b", "C4"])
+def test_speculative_capacity_rarely_falls_back(name):
+    """Cost guard on the speculative capacities: at every
+    bench workload's launch configuration at most 1% of the replications
+    overflow the main launch and re-run in the fallback launch
+    (`launch_info()["last_retries"]`).  Rows are bit-exact either way; a
+    systematic overflow doubles the cost (C3a_tv FCFS once re-ran all 10^4:
+    117 vs 47 ms)."""
+    import importlib.util
+    import os
+    from paper_2504_11320_b200 import Scheduler
+    from paper_2504_11320_b200.sim import run_rows
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    pols, reps, _ = bench.expand(name)
+    for label, pol, thr, wl in pols:
+        s = Scheduler(wl, pol, thr, **bench.SCHED_KW.get(name, {}))
+        if thr is None and pol.kind in (W.WAIT, W.NESTED):
+            s.thresholds()
+        rows = run_rows(s, wl.seed, 0, reps, wl.horizon_s)
+        torch.cuda.synchronize()
+        li = s.launch_info()
+        s.close()
+        assert int((rows[oracle.F["status"]] != 0).sum().item()) == 0, label
+        assert li["last_retries"] <= reps // 100, f"{name}/{label}: {li['last_retries']} of {reps} re-ran"

@@ -19,6 +19,9 @@ if wl_name == "C2":
     wl, pols = W.C2, [W.Policy(W.WAIT), W.Policy(W.FCFS, B=1024)]
 elif wl_name == "C3a":
     wl, pols = W.C3A, [W.Policy(W.NESTED, seg_end=[20, 40, 80, 160]), W.Policy(W.FCFS, B=1024)]
+elif wl_name == "C3a_tv":
+    wl, pols = W.c3a_time_varying(), [W.Policy(W.NESTED, seg_end=[20, 40, 80, 160], thresholds=[11, 11, 10, 7]),
+                                      W.Policy(W.FCFS, B=1024)]
 elif wl_name.startswith("C4_"):
     wl = W.c4(int(wl_name[3:]))
     pols = [W.Policy(W.WAIT), W.Policy(W.NESTED, seg_end=[100, 200, 300]), W.Policy(W.FCFS, B=1024)]
@@ -30,6 +33,8 @@ R = int(os.environ.get("REPS", "10000"))
 T = float(os.environ.get("HORIZON", str(wl.horizon_s)))
 for pol in pols:
     kw = {}
+    if os.environ.get("POLS") and W.POLICY_NAMES[pol.kind] not in os.environ["POLS"].split(","):
+        continue
     if os.environ.get("RCAP"):
         kw["restart_cap"] = int(os.environ["RCAP"])
     if os.environ.get("MAXRES"):
@@ -53,4 +58,4 @@ for pol in pols:
     li = s.launch_info()
     print(f"{wl_name} {W.POLICY_NAMES[pol.kind]:6s} ms={min(ts):8.3f} rs/s={rs/min(ts)*1e3:.3e} status!=0:{st} "
           f"wpb={li['warps_per_block']} bps={li['blocks_per_sm']} spec={li['spec_resident']} safe={li['max_resident']} "
-          f"smem={li['shared_bytes']} fb={li['fallback_grid']} eng={li.get('engine', 0)}")
+          f"smem={li['shared_bytes']} fb={li['fallback_grid']} eng={li.get('engine', 0)} retries={li.get('last_retries', -1)}")
