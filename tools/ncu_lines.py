@@ -53,7 +53,7 @@ for k, lines in agg.items():
         byf = defaultdict(lambda: [0, 0])
         for (f, ln), (s, i, _) in lines.items():
             name = f
-            if f == "sim_kernel.cu":
+            if f.startswith("sim_kernel.cu"):
                 name = "other"
                 for n, lo, hi in regions:
                     if lo <= ln <= hi:
