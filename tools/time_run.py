@@ -32,7 +32,7 @@ else:
 R = int(os.environ.get("REPS", "10000"))
 T = float(os.environ.get("HORIZON", str(wl.horizon_s)))
 for pol in pols:
-    kw = {}
+    kw = dict(max_resident=4096, restart_cap=2_000_000_000) if wl_name.startswith("C5") else {}  # as bench.py
     if os.environ.get("POLS") and W.POLICY_NAMES[pol.kind] not in os.environ["POLS"].split(","):
         continue
     if os.environ.get("RCAP"):
