@@ -37,6 +37,8 @@ for pol in pols:
         continue
     if os.environ.get("RCAP"):
         kw["restart_cap"] = int(os.environ["RCAP"])
+    if os.environ.get("SPEC"):
+        kw["spec_resident"] = int(os.environ["SPEC"])
     if os.environ.get("MAXRES"):
         kw["max_resident"] = int(os.environ["MAXRES"])
     s = Scheduler(wl, pol, pol.thresholds, **kw)
