@@ -451,13 +451,33 @@ int prepare(sched_s* h) {
     L = LaunchCfg{};
     L.seg = true;
     L.Rc = L.Rc_safe = round32(h->in.thresholds[0]);  // staged admissions: n_1 per batch
-    double f = 1.5;
-    if (const char* fs = getenv("WAITSIM_SEG_CAP")) f = std::max(0.1, atof(fs));
-    // the member engine's speculative population (live residents) x f:
-    // room for the tombstones of mid-segment completions between compactions
-    L.seg_cap = round32((uint64_t)(f * h->mem.Rc) + 2ull * h->in.thresholds[0]);
-    int wpb = 1, bps = 0;
-    if (size_launch(false, L.Rc, &L.warp_smem, &wpb, &bps, L.seg_cap) == 0) {
+    // array capacity = the member engine's speculative population (live
+    // residents) x f + two admission batches: room for the tombstones of
+    // mid-segment completions between compactions.  f in [1.2, 1.5]: the
+    // largest capacity among those reaching the most resident warps per SM
+    // (shared memory bounds the engine's occupancy; measured C3a 10 -> 12
+    // warps 59.4 -> 54.3 ms, C3b 6 -> 8 warps 21.7 -> 17.3 ms; f = 1.0 already
+    // overflows 16% of C3a's replications into the fallback launch)
+    auto cap_of = [&](double f) {
+      return round32((uint64_t)(f * h->mem.Rc) + 2ull * h->in.thresholds[0]);
+    };
+    int wpb = 1, bps = 0, best = -1;
+    uint32_t wsm = 0;
+    const char* fs = getenv("WAITSIM_SEG_CAP");
+    const bool fixed_f = fs || h->spec_resident_cfg;  // forced, or an explicit speculative capacity: f = 1.5
+    for (int step = 0; step <= (fixed_f ? 0 : 15); ++step) {
+      const uint32_t cap = fs ? cap_of(std::max(0.1, atof(fs))) : cap_of(1.5 - 0.02 * step);  // step 0: f = 1.5
+      int w = 1, b = 0;
+      if (size_launch(false, L.Rc, &wsm, &w, &b, cap) != 0) continue;
+      if (w * b > best) {
+        best = w * b;
+        wpb = w;
+        bps = b;
+        L.seg_cap = cap;
+        L.warp_smem = wsm;
+      }
+    }
+    if (best > 0) {
       L.wpb = wpb;
       L.blocks_per_sm = bps;
       L.block = wpb * 32;
