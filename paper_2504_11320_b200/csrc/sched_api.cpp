@@ -294,7 +294,7 @@ int prepare(sched_s* h) {
       if (smem > (size_t)prop.sharedMemPerBlockOptin) continue;
       // max blocks per SM from shared memory and registers (occupancy API)
       int bps = 0;
-      const cudaError_t e = sim_occupancy(h->in.policy, 0, wpb * 32, smem, &bps, seg_cap ? 2 : ring ? 1 : 0);
+      const cudaError_t e = sim_occupancy(h->in.policy, 0, wpb * 32, smem, &bps, seg_cap ? 2 : ring ? 1 : 0, K);
       if (e != cudaSuccess) return cuda_fail(e, "occupancy");
       if (bps * wpb > best_w) { best_w = bps * wpb; *wpb_out = wpb; *bps_out = bps; }
     }

@@ -15,7 +15,9 @@ cudaError_t launch_member(const DevParams& p, int grid, int block, size_t smem, 
   }
 }
 
-cudaError_t occ_member(int policy, int block, size_t smem, int* bps) {
+cudaError_t occ_member(int policy, int K, int block, size_t smem, int* bps) {
+  if (K == 1 && policy == SCHED_NESTED) return occ_t<SCHED_NESTED, false, false, false, 1>(block, smem, bps);
+  if (K == 1 && policy == SCHED_FCFS) return occ_t<SCHED_FCFS, false, false, false, 1>(block, smem, bps);
   switch (policy) {
     case SCHED_WAIT: return occ_t<SCHED_WAIT, false>(block, smem, bps);
     case SCHED_NESTED: return occ_t<SCHED_NESTED, false>(block, smem, bps);

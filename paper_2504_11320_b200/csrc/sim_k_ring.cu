@@ -27,7 +27,22 @@ cudaError_t launch_ring(const DevParams& p, int grid, int block, size_t smem, cu
   }
 }
 
-cudaError_t occ_ring(int policy, int block, size_t smem, int* bps) {
+cudaError_t occ_ring(int policy, int K, int block, size_t smem, int* bps) {
+  // the kernel launch_ring runs (its launch bound can depend on K)
+  if (policy == SCHED_WAIT || policy == SCHED_FCFS) {
+    const bool w = policy == SCHED_WAIT;
+    switch (K) {
+      case 1: return w ? occ_t<SCHED_WAIT, false, true, false, 1>(block, smem, bps)
+                       : occ_t<SCHED_FCFS, false, true, false, 1>(block, smem, bps);
+      case 2: return w ? occ_t<SCHED_WAIT, false, true, false, 2>(block, smem, bps)
+                       : occ_t<SCHED_FCFS, false, true, false, 2>(block, smem, bps);
+      case 3: return w ? occ_t<SCHED_WAIT, false, true, false, 3>(block, smem, bps)
+                       : occ_t<SCHED_FCFS, false, true, false, 3>(block, smem, bps);
+      case 4: return w ? occ_t<SCHED_WAIT, false, true, false, 4>(block, smem, bps)
+                       : occ_t<SCHED_FCFS, false, true, false, 4>(block, smem, bps);
+      default: break;
+    }
+  }
   switch (policy) {
     case SCHED_WAIT: return occ_t<SCHED_WAIT, false, true>(block, smem, bps);
     case SCHED_FCFS_ONGOING: return occ_t<SCHED_FCFS_ONGOING, false, true>(block, smem, bps);

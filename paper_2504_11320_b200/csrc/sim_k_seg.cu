@@ -10,7 +10,9 @@ cudaError_t launch_seg(const DevParams& p, int grid, int block, size_t smem, cud
   return launch_t<SCHED_NESTED, false, false, true>(p, grid, block, smem, s);
 }
 
-cudaError_t occ_seg(int block, size_t smem, int* bps) {
+cudaError_t occ_seg(int K, int block, size_t smem, int* bps) {
+  if (K == 1) return occ_t<SCHED_NESTED, false, false, true, 1>(block, smem, bps);
+  if (K == 4) return occ_t<SCHED_NESTED, false, false, true, 4>(block, smem, bps);
   return occ_t<SCHED_NESTED, false, false, true>(block, smem, bps);
 }
 

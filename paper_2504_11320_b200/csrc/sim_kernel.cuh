@@ -33,6 +33,10 @@
 #include "../../include/sched.h"
 #include "sim_internal.h"
 
+#ifndef WAITSIM_FCFS2_MINB  // experiment knob (measured: 6 -> C2 FCFS 15.6 -> 18.5 ms)
+#define WAITSIM_FCFS2_MINB 5
+#endif
+
 namespace waitsim {
 namespace {
 
@@ -2438,13 +2442,24 @@ struct WarpSim {
   }
 };
 
+// blocks per SM the register allocation is sized for (launch bound): the
+// two-class WAIT ring kernel runs best at 6 x 4 warps / 80 registers despite
+// 72 B of spills (C2 WAIT 13.7 -> 13.0 ms; K = 1 and 3 lose at 6: C1 +1%,
+// C4 rho=0.95 +7%), the other WAIT / class-ring kernels at 5 x 4 / 96
+template <int POL, bool RING, int KC>
+constexpr int kMinBlocks() {
+  return (POL == SCHED_WAIT && RING && KC == 2) ? 6
+       : (POL == SCHED_FCFS && RING && KC == 2) ? WAITSIM_FCFS2_MINB
+       : (POL == SCHED_WAIT || RING) ? 5 : 2;
+}
+
 template <int POL, bool TRACE, bool RING, bool SEG, int KC>
 // WAIT and the class-ring engine: <= 4 warps per block, 5 blocks per SM ->
 // <= 102 registers, 20 warps/SM (the ring engine's shared footprint is small,
 // so registers bound its occupancy: measured C2 FCFS 128 registers / 16
 // warps 20.9 ms -> 96 / 20 warps 18.7 ms; 80 / 24 warps spills, 20.7 ms);
 // the member and segment engines are shared-memory bound: 128 registers
-__global__ void __launch_bounds__((POL == SCHED_WAIT || RING) ? 128 : 256, (POL == SCHED_WAIT || RING) ? 5 : 2)
+__global__ void __launch_bounds__((POL == SCHED_WAIT || RING) ? 128 : 256, kMinBlocks<POL, RING, KC>())
     sim_kernel(const DevParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int wib = threadIdx.x >> 5;

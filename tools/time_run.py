@@ -17,6 +17,8 @@ wl_name = os.environ.get("WL", "C2")
 seg10 = [50 * k for k in range(1, 11)]
 if wl_name == "C2":
     wl, pols = W.C2, [W.Policy(W.WAIT), W.Policy(W.FCFS, B=1024)]
+elif wl_name == "C1":
+    wl, pols = W.C1, [W.Policy(W.WAIT), W.Policy(W.FCFS, B=32), W.Policy(W.NESTED, seg_end=[16], thresholds=[1])]
 elif wl_name == "C3a":
     wl, pols = W.C3A, [W.Policy(W.NESTED, seg_end=[20, 40, 80, 160]), W.Policy(W.FCFS, B=1024)]
 elif wl_name == "C3a_tv":
