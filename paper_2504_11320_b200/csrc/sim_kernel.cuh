@@ -1081,13 +1081,13 @@ struct WarpSim {
       if (m == 0) break;
       if (base + m > P.Rc) { status = 1; return false; }
       // (2) rank candidates; rank < m -> staged at slot base + rank
-      if (POL == SCHED_WAIT) {
-        // WAIT: FIFO q = class q + its restarts; lane i holds arrival i
+      if (POL == SCHED_WAIT || (POL != SCHED_NESTED && KC == 1)) {
+        // WAIT (FIFO q = class q + its restarts) or one-class FCFS: lane i holds arrival i
         // and restart i; both sources are sorted (ticks; eviction ticks in
         // FIFO order), so each rank is i + a count in the other source,
         // found by a branch-free binary search over lanes (shuffles).  A
         // restart evicted at e precedes exactly the arrivals with t > e
-        // (DESIGN.md §4.4).  The restarts' pool records are requested before
+        // (DESIGN.md §4.4).  C1 FCFS 85.6 -> 71.5 ms.  The restarts' pool records are requested before
         // the search so their latency overlaps it.  (C4 rho = 0.9 / 0.95 WAIT
         // 2.86 / 1.93 -> 2.49 / 1.83 ms; the same merge for Nested K = 1 lost:
         // C5 584 -> 622 ms.)
