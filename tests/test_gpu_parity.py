@@ -400,7 +400,7 @@ def test_idle_skip_partial_jumps():
 
 def test_engine_selection_rule(monkeypatch):
     """the class-ring engine for every fixed-length WAIT /
-    FCFS configuration (its member records live in global memory, so its
+    FCFS configuration (and one-class one-segment Nested, P10) (its member records live in global memory, so its
     footprint no longer depends on the population), the segment engine for
     Nested except one segment or decode-length marks with M^pi > M (member
     engine, measured faster there), the member engine for length marks under
@@ -413,7 +413,9 @@ def test_engine_selection_rule(monkeypatch):
     assert eng(W.C3A, W.Policy(W.NESTED, seg_end=SEG3A), [7, 7, 7, 5]) == 2
     assert eng(W.C3B, W.Policy(W.NESTED, seg_end=SEG10), fl.nested_strict(W.C3B, SEG10)) == 2
     assert eng(W.c4(4), W.Policy(W.NESTED, seg_end=SEG4), [46, 23, 8]) == 2
-    assert eng(W.C1, W.Policy(W.NESTED, seg_end=[16]), [1]) == 0          # one segment
+    # one class, one segment: Nested IS WAIT with one type (P10, pinned on the
+    # oracle) -> its runs go to a WAIT twin handle on the class-ring engine
+    assert eng(W.C1, W.Policy(W.NESTED, seg_end=[16]), [1]) == 1
     assert eng(W.c5(55.0), W.Policy(W.NESTED, seg_end=SEG10), [11, 8, 6, 5, 4, 3, 2, 2, 2, 2]) == 0  # marks, M^pi > M
     monkeypatch.setenv("WAITSIM_ENGINE", "member")
     assert eng(W.C3A, W.Policy(W.NESTED, seg_end=SEG3A), [7, 7, 7, 5]) == 0
@@ -624,3 +626,28 @@ def test_speculative_capacity_rarely_falls_back(name):
         s.close()
         assert int((rows[oracle.F["status"]] != 0).sum().item()) == 0, label
         assert li["last_retries"] <= reps // 100, f"{name}/{label}: {li['last_retries']} of {reps} re-ran"
+
+
+def test_one_segment_nested_runs_as_wait(monkeypatch):
+    """P10 routing: a one-class one-segment Nested handle runs on its WAIT twin
+    (class-ring engine); rows are bit-identical to the oracle's Nested rows and
+    to the same handle forced onto the Nested member engine, with thresholds
+    installed by sched_thresholds after creation."""
+    from paper_2504_11320_b200 import Scheduler
+    monkeypatch.delenv("WAITSIM_ENGINE", raising=False)
+    pol = W.Policy(W.NESTED, seg_end=[16])
+    for thr in ([1], [2], None):
+        s = Scheduler(W.C1, pol, thr)
+        th = thr if thr is not None else s.thresholds()["thresholds"]
+        assert s.launch_info()["engine"] == 1
+        got = s.run_host(W.C1.seed, 5, 64, 8.0)
+        assert s.status_mask() == 0
+        s.close()
+        ref = oracle.run(W.C1, pol, th, n_reps=64, rep_begin=5, n_threads=8, horizon_s=8.0)
+        assert_rows_equal(got, ref, f"nested one segment thr={th}")
+        monkeypatch.setenv("WAITSIM_ENGINE", "member")
+        s = Scheduler(W.C1, pol, th)
+        assert s.launch_info()["engine"] == 0
+        assert_rows_equal(s.run_host(W.C1.seed, 5, 64, 8.0), ref, "member engine")
+        s.close()
+        monkeypatch.delenv("WAITSIM_ENGINE")
