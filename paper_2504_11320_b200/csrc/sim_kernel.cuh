@@ -690,10 +690,11 @@ struct WarpSim {
   }
 
   __device__ void ingest() {
-    // specialised FCFS: both classes unrolled (offsets are immediates; C2 FCFS
-    // 16.8 -> 15.7 ms, spills 220 -> 108 B).  Not WAIT: it inlines the window
+    // specialised FCFS, K <= 3: the classes unrolled (offsets are immediates;
+    // C2 FCFS 16.8 -> 15.7 ms, spills 220 -> 108 B; C4 K = 3 -3%; K = 4 loses:
+    // C3a FCFS 52 -> 62 ms).  Not WAIT: it inlines the window
     // generator, and two inlined copies cost more than they save (13.7 -> 15.1 ms)
-    if (KC > 0 && KC <= 2 && POL != SCHED_WAIT) {
+    if (KC > 0 && KC <= 3 && POL != SCHED_WAIT) {
       uint32_t n = 0;
 #pragma unroll
       for (int c = 0; c < KC; ++c) n += ingest_class<true>(c);
