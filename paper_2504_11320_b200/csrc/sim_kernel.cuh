@@ -33,8 +33,18 @@
 #include "../../include/sched.h"
 #include "sim_internal.h"
 
-#ifndef WAITSIM_FCFS2_MINB  // experiment knob (measured: 6 -> C2 FCFS 15.6 -> 18.5 ms)
+// launch-bound knobs of the FCFS class-ring kernels (blocks per SM), measured:
+// K = 2: 5 (6: C2 FCFS 15.6 -> 18.5 ms, 4: -> 17.4 ms); K = 3: 4 (C4 FCFS
+// 2.65 / 2.91 -> 2.55 / 2.75 ms at rho 0.9 / 0.95); K = 4: 5 (4: C3a FCFS
+// 51.9 -> 54.6 ms)
+#ifndef WAITSIM_FCFS2_MINB
 #define WAITSIM_FCFS2_MINB 5
+#endif
+#ifndef WAITSIM_FCFS3_MINB
+#define WAITSIM_FCFS3_MINB 4
+#endif
+#ifndef WAITSIM_FCFS4_MINB
+#define WAITSIM_FCFS4_MINB 5
 #endif
 
 namespace waitsim {
@@ -2451,6 +2461,8 @@ template <int POL, bool RING, int KC>
 constexpr int kMinBlocks() {
   return (POL == SCHED_WAIT && RING && KC == 2) ? 6
        : (POL == SCHED_FCFS && RING && KC == 2) ? WAITSIM_FCFS2_MINB
+       : (POL == SCHED_FCFS && RING && KC == 3) ? WAITSIM_FCFS3_MINB
+       : (POL == SCHED_FCFS && RING && KC == 4) ? WAITSIM_FCFS4_MINB
        : (POL == SCHED_WAIT || RING) ? 5 : 2;
 }
 
