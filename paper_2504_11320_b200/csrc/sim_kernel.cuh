@@ -791,11 +791,12 @@ struct WarpSim {
   // the longest prefix passing the test of PAPER.md:1427, 1745 (R15)
   __device__ __forceinline__ uint32_t fcfs_take(uint32_t m, uint32_t l) const {
     const uint32_t pre = warp_incl_scan_u32(l, lane);
-    const bool ok = (uint32_t)lane < m && (n_res + n_new + lane < P.B) &&
-                    // Sarathi-style ongoing-first also reserves the residents' growth (R29)
-                    (KV + (POL == SCHED_FCFS_ONGOING ? (int64_t)n_res : 0) + sum_new_l +
-                         (int64_t)pre <= P.M) &&
-                    (P.tok_budget == 0 || sum_new_l + (int64_t)pre <= (int64_t)P.tok_budget);
+    // uniform limits: KV room (Sarathi-style ongoing-first also reserves the
+    // residents' growth, R29), prefill-token budget, resident slots
+    int64_t room = P.M - KV - (POL == SCHED_FCFS_ONGOING ? (int64_t)n_res : 0) - sum_new_l;
+    if (P.tok_budget) room = min(room, (int64_t)P.tok_budget - sum_new_l);
+    const uint32_t used = n_res + n_new, slots = P.B > used ? P.B - used : 0u;
+    const bool ok = (uint32_t)lane < min(m, slots) && (int64_t)pre <= room;
     const uint32_t okm = __ballot_sync(FULL, ok);  // ok lanes form a prefix
     return okm == FULL ? 32u : (uint32_t)__ffs(~okm) - 1;
   }
