@@ -37,6 +37,9 @@
 // K = 2: 5 (6: C2 FCFS 15.6 -> 18.5 ms, 4: -> 17.4 ms); K = 3: 4 (C4 FCFS
 // 2.65 / 2.91 -> 2.55 / 2.75 ms at rho 0.9 / 0.95); K = 4: 5 (4: C3a FCFS
 // 51.9 -> 54.6 ms)
+#ifndef WAITSIM_MEMBER_FCFS_MINB  // member-engine FCFS (length marks), blocks of 8 warps: 3 (80
+#define WAITSIM_MEMBER_FCFS_MINB 3   // registers): C3b FCFS 32.6 -> 30.1 ms, C5 FCFS 68 -> 71 ms per 600 s
+#endif
 #ifndef WAITSIM_FCFS2_MINB
 #define WAITSIM_FCFS2_MINB 5
 #endif
@@ -2464,7 +2467,8 @@ constexpr int kMinBlocks() {
        : (POL == SCHED_FCFS && RING && KC == 2) ? WAITSIM_FCFS2_MINB
        : (POL == SCHED_FCFS && RING && KC == 3) ? WAITSIM_FCFS3_MINB
        : (POL == SCHED_FCFS && RING && KC == 4) ? WAITSIM_FCFS4_MINB
-       : (POL == SCHED_WAIT || RING) ? 5 : 2;
+       : (POL == SCHED_WAIT || RING) ? 5
+       : (POL == SCHED_FCFS) ? WAITSIM_MEMBER_FCFS_MINB : 2;  // member engine (FCFS never uses SEG)
 }
 
 template <int POL, bool TRACE, bool RING, bool SEG, int KC>
