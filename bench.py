@@ -554,7 +554,7 @@ def bench_strong(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": pkg.NF * 8 * n * len(scheds),
                 "note": "one sweep through sched_run_host (launch + D2H of the rows + sync per point)"},
-        "gpu_launches": sum(1 + (1 if s.launch_info()["fallback_grid"] else 0) for _, s, _ in scheds) * args.steps,
+        "gpu_launches": sum(2 + (1 if s.launch_info()["fallback_grid"] else 0) for _, s, _ in scheds) * args.steps,
         "kernel_ms_to_end": {lb: 1e3 * sum(v) / len(v) for lb, v in t_kern.items()},
         "clocks": clk,
     }
@@ -748,7 +748,8 @@ def main():
                 "d2h_bytes_per_step": pkg.NF * R * 8 * len(scheds),
                 "note": "sched_run_host: launch + D2H of the metric rows + sync; the step's inputs are "
                         "seeds and replication indices (kernel arguments), so no H2D input bytes"},
-        "gpu_launches": sum(1 + (1 if s.launch_info()["fallback_grid"] else 0) for _, s, _ in scheds)
+        # per policy and step: the simulation, its fallback launch (if any), sched_aggregate
+        "gpu_launches": sum(2 + (1 if s.launch_info()["fallback_grid"] else 0) for _, s, _ in scheds)
         * args.steps,
         "roofline": roof,
         "hbm": roof.pop("hbm"),

@@ -193,6 +193,23 @@ int sched_run(sched_t h, uint64_t seed, uint64_t rep_begin, uint32_t n_reps,
 int sched_run_host(sched_t h, uint64_t seed, uint64_t rep_begin, uint32_t n_reps,
                    double horizon_s, uint64_t* out_host, void* cuda_stream);
 
+/* Sums over the replications of one run (the per-policy vector that the
+ * cross-GPU all-reduce adds; metrics of PAPER.md:1235-1242), on the device,
+ * asynchronous on `cuda_stream`.  rows_dev: DEVICE field-major rows as
+ * written by sched_run, field f of replication i at rows_dev[f*ld + i]
+ * (ld >= n_reps: a column slice of a wider array).  out_int_dev (13 int64):
+ * sums of ARRIVALS, ADMITTED, COMPLETED, COMPLETED_AFTER_T, COMPLETED_TOKENS,
+ * FIRST_TOKENS, BATCHES, REQUEST_STEPS, PREFILL_STEPS, EVICTIONS,
+ * FINAL_WAITING, FINAL_RESIDENT, and the number of replications with
+ * STATUS != 0.  out_f64_dev (6 double): sum of latency, TTFT and sojourn
+ * tick sums and BUSY_TICKS in seconds, sum over replications of (latency
+ * sum / max(COMPLETED, 1))^2 and of (COMPLETED_TOKENS / horizon_s)^2.  One
+ * 1024-thread block, fixed summation order (deterministic).  Errors:
+ * SCHED_E_INVALID (null pointer, n_reps == 0, ld < n_reps, horizon <= 0),
+ * SCHED_E_CUDA (launch failure). */
+int sched_aggregate(const uint64_t* rows_dev, uint64_t ld, uint32_t n_reps, double horizon_s,
+                    int64_t* out_int_dev, double* out_f64_dev, void* cuda_stream);
+
 /* Explicit arrival traces (host arrays): replication i replays arrivals
  * [off[i], off[i+1]) of (t_ticks, cls, l, lp), sorted by (t, cls).  Rows go
  * to out_host (SCHED_NF * n_reps, field-major); if log_host != NULL the

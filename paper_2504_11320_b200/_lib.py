@@ -30,7 +30,7 @@ NF = len(FIELDS)
 F = {n: i for i, n in enumerate(FIELDS)}
 
 # every symbol include/sched.h declares
-EXPORTS = ["sched_create", "sched_thresholds", "sched_run", "sched_run_host",
+EXPORTS = ["sched_create", "sched_thresholds", "sched_run", "sched_run_host", "sched_aggregate",
            "sched_run_trace", "sched_get_launch_info", "sched_get_status", "sched_restart_pool_stats",
            "sched_walks", "sched_walks_host", "sched_destroy", "sched_last_error"]
 WALK_FIELDS = ["W_B", "stuck", "sumW", "maxW", "Wt_B", "viol", "sumX", "maxS", "minS", "S_B"]
@@ -103,6 +103,8 @@ def lib() -> C.CDLL:
         L.sched_run_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_uint32, C.c_double, C.c_void_p, C.c_void_p,
                                       C.c_int64, C.POINTER(C.c_int64)]
+        L.sched_aggregate.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_double, C.c_void_p, C.c_void_p,
+                                      C.c_void_p]
         L.sched_get_launch_info.argtypes = [C.c_void_p, C.POINTER(LaunchInfo)]
         L.sched_restart_pool_stats.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.sched_get_status.argtypes = [C.c_void_p, C.POINTER(C.c_uint32)]
@@ -113,7 +115,7 @@ def lib() -> C.CDLL:
         L.sched_walks_host.argtypes = [C.c_int32, C.c_int64, C.c_double, C.c_int64, C.c_double,
                                        C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p,
                                        C.c_int32]
-        for name in ["sched_create", "sched_thresholds", "sched_run", "sched_run_host",
+        for name in ["sched_create", "sched_thresholds", "sched_run", "sched_run_host", "sched_aggregate",
                      "sched_run_trace", "sched_get_launch_info", "sched_restart_pool_stats",
                      "sched_get_status", "sched_walks", "sched_walks_host"]:
             getattr(L, name).restype = C.c_int
@@ -293,6 +295,13 @@ def walks(kind: int, n: int, B: int, n_walks: int, seed: int, walk_begin: int = 
     _check(lib().sched_walks_host(kind, n, mu, n_prev, p, seed, walk_begin, n_walks, B,
                                   out.ctypes.data, device))
     return out
+
+
+def aggregate_device(rows_ptr: int, ld: int, n_reps: int, horizon_s: float, out_int_ptr: int,
+                     out_f64_ptr: int, stream_ptr: int = 0):
+    """sched_aggregate: asynchronous device-side sums of one run's rows."""
+    _check(lib().sched_aggregate(C.c_void_p(rows_ptr), ld, n_reps, horizon_s, C.c_void_p(out_int_ptr),
+                                 C.c_void_p(out_f64_ptr), C.c_void_p(stream_ptr)))
 
 
 def walks_device(kind: int, n: int, B: int, n_walks: int, seed: int, out_ptr: int,

@@ -41,8 +41,20 @@ AGG_INT = ["arrivals", "admitted", "completed", "completed_after_T", "completed_
 AGG_F64 = ["lat", "ttft", "soj", "busy", "lat_sq", "thr_sq"]
 
 
-def aggregate(rows: torch.Tensor, horizon_s: float) -> Dict[str, torch.Tensor]:
-    """Device-side sums over replications of one rows tensor (small vectors)."""
+def aggregate(rows: torch.Tensor, horizon_s: float, stream: torch.cuda.Stream = None) -> Dict[str, torch.Tensor]:
+    """Sums over replications of one rows tensor [NF, n] (small vectors).
+    Device rows: one libsched kernel (sched_aggregate, asynchronous on
+    `stream`).  Host rows (the CPU process-group tests feed oracle rows): the
+    same definition in torch ops."""
+    if rows.is_cuda:
+        from ._lib import aggregate_device
+        assert rows.dtype == torch.int64 and rows.shape[0] == NF and rows.stride(1) == 1
+        out_i = torch.empty(len(AGG_INT), dtype=torch.int64, device=rows.device)
+        out_f = torch.empty(len(AGG_F64), dtype=torch.float64, device=rows.device)
+        st = stream if stream is not None else torch.cuda.current_stream(rows.device)
+        aggregate_device(rows.data_ptr(), rows.stride(0), rows.shape[1], horizon_s, out_i.data_ptr(),
+                         out_f.data_ptr(), st.cuda_stream)
+        return {"int": out_i, "f64": out_f}
     r = rows
     # status: the NUMBER of replications with a nonzero status (1 resident
     # overflow, 2 restart overflow), not the sum of the codes

@@ -98,3 +98,25 @@ def test_two_ranks_gloo_on_device_tensors():
     for _, ints, f64 in res:
         assert ints == ref["int"].tolist()
         assert np.allclose(f64, ref["f64"].numpy(), rtol=1e-12)
+
+
+def test_aggregate_kernel_matches_definition_on_slices():
+    """sched_aggregate on a column slice (row stride > n_reps) of random rows,
+    some with a nonzero status: integer sums exact, float sums within 1e-12
+    relative of the torch definition on the same rows (host)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2504_11320_b200.sim import NF, F, aggregate
+    g = np.random.default_rng(7)
+    full = g.integers(0, 1 << 40, size=(NF, 4096), dtype=np.int64)
+    for f in ("lat_hi", "ttft_hi", "soj_hi"):
+        full[F[f]] = g.integers(0, 3, size=4096)
+    full[F["status"]] = g.integers(0, 3, size=4096) * (g.random(4096) < 0.1)
+    full[F["completed"], :7] = 0  # mean latency divides by max(completed, 1)
+    dev = torch.from_numpy(full).cuda()
+    for lo, n in [(0, 1), (5, 300), (100, 3996)]:
+        got = aggregate(dev[:, lo:lo + n], 10.0)
+        torch.cuda.synchronize()
+        ref = aggregate(torch.from_numpy(np.ascontiguousarray(full[:, lo:lo + n])), 10.0)
+        assert got["int"].cpu().tolist() == ref["int"].tolist(), (lo, n)
+        assert np.allclose(got["f64"].cpu().numpy(), ref["f64"].numpy(), rtol=1e-12, atol=0), (lo, n)
