@@ -2468,7 +2468,7 @@ constexpr int kMinBlocks() {
        : (POL == SCHED_FCFS && RING && KC == 3) ? WAITSIM_FCFS3_MINB
        : (POL == SCHED_FCFS && RING && KC == 4) ? WAITSIM_FCFS4_MINB
        : (POL == SCHED_WAIT || RING) ? 5
-       : (POL == SCHED_FCFS) ? WAITSIM_MEMBER_FCFS_MINB : 2;  // member engine (FCFS never uses SEG)
+       : (POL == SCHED_FCFS && KC == 1) ? WAITSIM_MEMBER_FCFS_MINB : 2;  // one-class member FCFS (marks)
 }
 
 template <int POL, bool TRACE, bool RING, bool SEG, int KC>
