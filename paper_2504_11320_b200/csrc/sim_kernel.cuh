@@ -37,6 +37,9 @@
 // K = 2: 5 (6: C2 FCFS 15.6 -> 18.5 ms, 4: -> 17.4 ms); K = 3: 4 (C4 FCFS
 // 2.65 / 2.91 -> 2.55 / 2.75 ms at rho 0.9 / 0.95); K = 4: 5 (4: C3a FCFS
 // 51.9 -> 54.6 ms)
+#ifndef WAITSIM_WAIT2_MINB  // two-class WAIT ring kernel: 6 (80 registers); 5: 13.7 ms, 7: 14.2 ms vs 13.0
+#define WAITSIM_WAIT2_MINB 6
+#endif
 #ifndef WAITSIM_MEMBER_FCFS_MINB  // member-engine FCFS (length marks), blocks of 8 warps: 3 (80
 #define WAITSIM_MEMBER_FCFS_MINB 3   // registers): C3b FCFS 32.6 -> 30.1 ms, C5 FCFS 68 -> 71 ms per 600 s
 #endif
@@ -2463,7 +2466,7 @@ struct WarpSim {
 // C4 rho=0.95 +7%), the other WAIT / class-ring kernels at 5 x 4 / 96
 template <int POL, bool RING, int KC>
 constexpr int kMinBlocks() {
-  return (POL == SCHED_WAIT && RING && KC == 2) ? 6
+  return (POL == SCHED_WAIT && RING && KC == 2) ? WAITSIM_WAIT2_MINB
        : (POL == SCHED_FCFS && RING && KC == 2) ? WAITSIM_FCFS2_MINB
        : (POL == SCHED_FCFS && RING && KC == 3) ? WAITSIM_FCFS3_MINB
        : (POL == SCHED_FCFS && RING && KC == 4) ? WAITSIM_FCFS4_MINB
