@@ -2154,14 +2154,28 @@ struct WarpSim {
       Rec e = {0, 0};
       if (v) e = rr[j];
       const uint32_t meta = (uint32_t)(e.q >> 48), c = v ? (meta & 0xFFu) : 0u;
-      const uint32_t grp = __match_any_sync(FULL, v ? c : 0x100u + (uint32_t)lane);
+      // lanes of the same class (rank within it) and, in lane c, class c's
+      // count of this chunk: one ballot per class when K is a constant
+      uint32_t grp = 0, add = 0;
+      if (KC > 0) {
+#pragma unroll
+        for (int cc = 0; cc < KC; ++cc) {
+          const uint32_t b = __ballot_sync(FULL, v && c == (uint32_t)cc);
+          if (c == (uint32_t)cc) grp = b;
+          if (lane == cc) add = __popc(b);
+        }
+      } else {
+        grp = __match_any_sync(FULL, v ? c : 0x100u + (uint32_t)lane);
+      }
       const uint32_t rk = __popc(grp & lanemask_lt());
       const uint32_t n = __shfl_sync(FULL, r_n, (int)c) + __shfl_sync(FULL, my_new, (int)c);
       const uint32_t head = __shfl_sync(FULL, r_head, (int)c);
       const uint32_t C = __shfl_sync(FULL, r_C, (int)c), cap = P.rcap[c];
       if (__any_sync(FULL, v && n + rk >= cap)) { status = 1; return false; }
-      cnt[lane] = 0;
-      __syncwarp();
+      if (KC == 0) {
+        cnt[lane] = 0;
+        __syncwarp();
+      }
       // a prompt without its first token emits it at the next participation
       const bool pend = v && !(meta & META_FT);
       if (v) {
@@ -2169,16 +2183,21 @@ struct WarpSim {
             make_ulonglong2((uint64_t)e.a | (pend ? 0ull : 1ull << 63), (unsigned long long)C);
         P.ring_log[(size_t)wslot * kRingLog + ((seq_next + j) & (kRingLog - 1))] = (uint8_t)c;
         acc_adm += (uint64_t)e.a;
-        if (rk == 0) cnt[c] = __popc(grp);
+        if (KC == 0 && rk == 0) cnt[c] = __popc(grp);
       }
       if (pend) {  // per-class pending first tokens (shared: pcnt = cnt[32..], psum)
         sh_add_u32(&cnt[32 + c], 1u);
         sh_add_u64(&psum()[c], (uint64_t)e.a);
       }
-      __syncwarp();
-      if (lane < nK()) my_new += cnt[lane];
-      __syncwarp();
+      if (KC > 0) {
+        my_new += add;
+      } else {
+        __syncwarp();
+        if (lane < nK()) my_new += cnt[lane];
+        __syncwarp();
+      }
     }
+    __syncwarp();
     if (lane < nK()) {
       r_n += my_new;
       r_X += (uint64_t)my_new * r_C;
