@@ -37,6 +37,13 @@
 // K = 2: 5 (6: C2 FCFS 15.6 -> 18.5 ms, 4: -> 17.4 ms); K = 3: 4 (C4 FCFS
 // 2.65 / 2.91 -> 2.55 / 2.75 ms at rho 0.9 / 0.95); K = 4: 5 (4: C3a FCFS
 // 51.9 -> 54.6 ms)
+// class count at which ring_append sums pending first tokens by ballot + warp
+// reductions instead of shared atomics (~15 same-address atomics per class and
+// batch at C2: WAIT 13.0 -> 12.3 ms, FCFS 15.4 -> 14.0 ms; K = 1 (C1: few
+// admissions per batch) +2%, K = 3 / 4 (C4 / C3a FCFS) +3 / +8%)
+#ifndef WAITSIM_PEND_REDUCE_K
+#define WAITSIM_PEND_REDUCE_K 2
+#endif
 #ifndef WAITSIM_WAIT2_MINB  // two-class WAIT ring kernel: 6 (80 registers); 5: 13.7 ms, 7: 14.2 ms vs 13.0
 #define WAITSIM_WAIT2_MINB 6
 #endif
@@ -2185,7 +2192,26 @@ struct WarpSim {
         acc_adm += (uint64_t)e.a;
         if (KC == 0 && rk == 0) cnt[c] = __popc(grp);
       }
-      if (pend) {  // per-class pending first tokens (shared: pcnt = cnt[32..], psum)
+      // per-class pending first tokens (shared: pcnt = cnt[32..], psum)
+      if (KC == WAITSIM_PEND_REDUCE_K) {
+        // per class: count by ballot, arrival-tick sum by three 32-bit warp
+        // reductions of 24-bit pieces (ticks < 2^57: every piece sum is exact)
+#pragma unroll
+        for (int cc = 0; cc < KC; ++cc) {
+          const bool mine = pend && c == (uint32_t)cc;
+          const uint32_t b = __ballot_sync(FULL, mine);
+          if (b) {
+            const uint64_t av = mine ? (uint64_t)e.a : 0ull;
+            const uint32_t s0 = __reduce_add_sync(FULL, (uint32_t)(av & 0xFFFFFFu));
+            const uint32_t s1 = __reduce_add_sync(FULL, (uint32_t)((av >> 24) & 0xFFFFFFu));
+            const uint32_t s2 = __reduce_add_sync(FULL, (uint32_t)(av >> 48));
+            if (lane == cc) {
+              cnt[32 + cc] += __popc(b);
+              psum()[cc] += (uint64_t)s0 + ((uint64_t)s1 << 24) + ((uint64_t)s2 << 48);
+            }
+          }
+        }
+      } else if (pend) {
         sh_add_u32(&cnt[32 + c], 1u);
         sh_add_u64(&psum()[c], (uint64_t)e.a);
       }
