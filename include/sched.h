@@ -232,8 +232,13 @@ typedef struct {
                                              FCFS with fixed per-class lengths; capacities
                                              then count ring + staging records); 2 segment
                                              engine (NESTED; spec_resident = its array,
-                                             fallback = the member engine's safe launch);
-                                             DESIGN.md §5.2.  The env var
+                                             fallback = the member engine's safe launch).
+                                             A NESTED handle with one class and one segment
+                                             is WAIT with one type (P10): its
+                                             sched_run calls execute on an internal WAIT
+                                             handle, so it reports that handle's launch
+                                             (engine 1 for fixed lengths); sched_run_trace
+                                             keeps the Nested engines.  DESIGN.md §5.2.  The env var
                                              WAITSIM_ENGINE=member|ring|seg, read when the
                                              handle is first launched, forces one. */
   int32_t last_retries;                   /* replications of the handle's most recent
