@@ -331,6 +331,11 @@ template <int POL, bool TRACE, bool RING, bool SEG, int KC>
 struct WarpSim {
   // class count: a compile-time constant when the kernel is specialised (KC > 0)
   __device__ __forceinline__ int nK() const { return KC ? KC : P.K; }
+  // the general admission path reads each staged restart's pool record in the
+  // same round trip as its eviction tick (C2 FCFS 14.1 -> 13.2 ms, C4 -1..3%);
+  // the Nested member engine and the four-class kernels keep the per-candidate
+  // reads (C5 Nested 588 -> 634 ms, C3a FCFS 49.4 -> 52.2 ms otherwise)
+  static constexpr bool kEarlyRestart = !(POL == SCHED_NESTED && !SEG) && KC != 4;
   const DevParams& P;
   const int lane;
   // shared-memory views (this warp's slice)
@@ -1092,9 +1097,21 @@ struct WarpSim {
       }
       const uint32_t nr = min(rcount(q), 32u);
       const uint32_t h0 = bcast32(rhead, q);
+      // lane i: restart i's eviction tick (to shared memory, for the ranks)
+      // and, in the same round trip, its arrival tick and lengths (shuffled
+      // to the candidate that stages it)
+      int64_t r_a = 0;
+      uint32_t r_llp = 0;
       if (nr > 0) {
         __syncwarp();
-        if ((uint32_t)lane < nr) re[lane] = __ldcg(P.pool_e + fifo_entry(q, h0 + lane));
+        if ((uint32_t)lane < nr) {
+          const size_t en = fifo_entry(q, h0 + lane);
+          re[lane] = __ldcg(P.pool_e + en);
+          if (kEarlyRestart) {
+            r_a = __ldcg(P.pool_a + en);
+            r_llp = __ldcg(P.pool_llp + en);
+          }
+        }
         __syncwarp();
       }
       const uint32_t ncand = total + nr;
@@ -1181,6 +1198,12 @@ struct WarpSim {
         const uint32_t s_o1 = __shfl_sync(FULL, my_o1, src & 31);
         const uint32_t s_n1 = __shfl_sync(FULL, my_n1, src & 31);
         const uint32_t s_priv = __shfl_sync(FULL, my_priv, src & 31);
+        int64_t ra_s = 0;
+        uint32_t rllp_s = 0;
+        if (kEarlyRestart) {
+          ra_s = __shfl_sync(FULL, r_a, (int)(pos & 31u));
+          rllp_s = __shfl_sync(FULL, r_llp, (int)(pos & 31u));
+        }
         int64_t key = 0, a = 0;
         uint32_t l = 0, lp = 0, meta = 0, r = pos;
         if (act) {
@@ -1199,9 +1222,13 @@ struct WarpSim {
             r += count_before(re, nr, key, false);       // restarts with e < t
           } else {
             key = re[pos];
-            const size_t e = fifo_entry(q, h0 + pos);
-            a = __ldcg(P.pool_a + e);
-            const uint32_t llp = __ldcg(P.pool_llp + e);
+            uint32_t llp = rllp_s;
+            a = ra_s;
+            if (!kEarlyRestart) {
+              const size_t e = fifo_entry(q, h0 + pos);
+              a = __ldcg(P.pool_a + e);
+              llp = __ldcg(P.pool_llp + e);
+            }
             uint32_t cls = POL == SCHED_WAIT ? (uint32_t)q : 0u;
             if (RING) {  // {class, ft}: the class fixes l, l'
               cls = llp & 0xFFu;
