@@ -72,11 +72,10 @@ __global__ void __launch_bounds__(1024) agg_kernel(const uint64_t* __restrict__ 
 }  // namespace
 }  // namespace waitsim
 
-extern "C" int sched_aggregate(const uint64_t* rows_dev, uint64_t ld, uint32_t n_reps, double horizon_s,
-                               int64_t* out_int_dev, double* out_f64_dev, void* cuda_stream) {
-  if (!rows_dev || !out_int_dev || !out_f64_dev || n_reps == 0 || ld < n_reps || !(horizon_s > 0))
-    return SCHED_E_INVALID;
-  waitsim::agg_kernel<<<1, 1024, 0, (cudaStream_t)cuda_stream>>>(rows_dev, ld, n_reps, horizon_s, out_int_dev,
-                                                                  out_f64_dev);
-  return cudaGetLastError() == cudaSuccess ? SCHED_OK : SCHED_E_CUDA;
+namespace waitsim {
+cudaError_t launch_aggregate(const uint64_t* rows, uint64_t ld, uint32_t n, double horizon_s, int64_t* out_i,
+                             double* out_f, cudaStream_t s) {
+  agg_kernel<<<1, 1024, 0, s>>>(rows, ld, n, horizon_s, out_i, out_f);
+  return cudaGetLastError();
 }
+}  // namespace waitsim

@@ -1045,6 +1045,16 @@ int sched_get_launch_info(sched_t h, sched_launch_info* out) {
   return SCHED_OK;
 }
 
+int sched_aggregate(const uint64_t* rows_dev, uint64_t ld, uint32_t n_reps, double horizon_s,
+                    int64_t* out_int_dev, double* out_f64_dev, void* cuda_stream) {
+  if (!rows_dev || !out_int_dev || !out_f64_dev) return fail(SCHED_E_INVALID, "null argument");
+  if (n_reps == 0) return fail(SCHED_E_INVALID, "n_reps must be > 0");
+  if (ld < n_reps) return fail(SCHED_E_INVALID, "row stride ld must be >= n_reps");
+  if (!(horizon_s > 0)) return fail(SCHED_E_INVALID, "horizon must be > 0");
+  CK(launch_aggregate(rows_dev, ld, n_reps, horizon_s, out_int_dev, out_f64_dev, (cudaStream_t)cuda_stream));
+  return SCHED_OK;
+}
+
 int sched_get_status(sched_t h, uint32_t* mask) {
   if (!h || !mask) return fail(SCHED_E_INVALID, "null argument");
   *mask = 0;

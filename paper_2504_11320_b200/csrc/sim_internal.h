@@ -134,6 +134,9 @@ inline uint32_t warp_smem_bytes(uint32_t Rc, int K, bool tv = false, bool ring =
 }
 
 cudaError_t launch_sim(const DevParams& p, int grid, int block, size_t smem, cudaStream_t s);
+// sched_aggregate's kernel (aggregate.cu): one 1024-thread block
+cudaError_t launch_aggregate(const uint64_t* rows, uint64_t ld, uint32_t n, double horizon_s, int64_t* out_i,
+                             double* out_f, cudaStream_t s);
 // blocks per SM of the kernel that launch_sim runs for (policy, engine, K)
 cudaError_t sim_occupancy(int policy, int trace, int block, size_t smem, int* blocks_per_sm, int ring = 0,
                           int K = 0);
