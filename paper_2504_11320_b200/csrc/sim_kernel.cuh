@@ -854,8 +854,9 @@ struct WarpSim {
     uint32_t l = 0;
     if ((uint32_t)lane < m) {
       const uint32_t idx = sg.at((uint32_t)lane);
-      l = vl[idx];
-      rr[base + lane] = Rec{vt[idx], pack_q(l, vlp[idx], 1, (uint32_t)c)};
+      // (class-ring engine: the class fixes l, l')
+      l = RING ? (P.fl[c] & 0xFFFFu) : vl[idx];
+      rr[base + lane] = Rec{vt[idx], pack_q(l, RING ? (P.fl[c] >> 16) : vlp[idx], 1, (uint32_t)c)};
     }
     const uint32_t take = FCFS_COND ? fcfs_take(m, l) : m;
     if (lane == c) { k_adm += take; newc += take; }
@@ -962,8 +963,11 @@ struct WarpSim {
       }
       r0 += i;
       r1 += i;
-      if (i < n[0] && r0 < m) rr[base + r0] = Rec{t0, pack_q(vl[i0], vlp[i0], 1, 0u)};
-      if (i < n[1] && r1 < m) rr[base + r1] = Rec{t1, pack_q(vl[i1], vlp[i1], 1, 1u)};
+      // (class-ring engine: the class fixes l, l' -- uniform constants, no window reads)
+      if (i < n[0] && r0 < m)
+        rr[base + r0] = Rec{t0, RING ? pack_q(P.fl[0] & 0xFFFFu, P.fl[0] >> 16, 1, 0u) : pack_q(vl[i0], vlp[i0], 1, 0u)};
+      if (i < n[1] && r1 < m)
+        rr[base + r1] = Rec{t1, RING ? pack_q(P.fl[1] & 0xFFFFu, P.fl[1] >> 16, 1, 1u) : pack_q(vl[i1], vlp[i1], 1, 1u)};
     } else {
 #pragma unroll
     for (int src = 0; src < KK; ++src) {
