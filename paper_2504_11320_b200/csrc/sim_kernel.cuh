@@ -41,6 +41,9 @@
 // reductions instead of shared atomics (~15 same-address atomics per class and
 // batch at C2: WAIT 13.0 -> 12.3 ms, FCFS 15.4 -> 14.0 ms; K = 1 (C1: few
 // admissions per batch) +2%, K = 3 / 4 (C4 / C3a FCFS) +3 / +8%)
+#ifndef WAITSIM_WAIT_GEN_INL  // WAIT kernels inline the window generator (1) or call it (0: C2 WAIT 12.3 -> 13.5 ms)
+#define WAITSIM_WAIT_GEN_INL 1
+#endif
 #ifndef WAITSIM_PEND_REDUCE_K
 #define WAITSIM_PEND_REDUCE_K 2
 #endif
@@ -648,7 +651,7 @@ struct WarpSim {
       return;
     }
     const ClassParam& cp = P.cls[c];
-    gen_window<POL == SCHED_WAIT>(lane, base, prev, rglob, (uint32_t)c, P.seed, cp.gap_scale, P.cdf_thr, P.cdf_val,
+    gen_window<POL == SCHED_WAIT && WAITSIM_WAIT_GEN_INL>(lane, base, prev, rglob, (uint32_t)c, P.seed, cp.gap_scale, P.cdf_thr, P.cdf_val,
                P.cdf_guide, cp.l_goff, cp.lp_goff, cp.l_off, cp.l_n, cp.lp_off, cp.lp_n, cp.rf_off, cp.rf_n, P.rf_B, P.rf_Lam,
                P.rf_scale, wt + c * 32, wl + c * 32, wlp + c * 32, wtau ? wtau + c * 32 : nullptr);
   }
