@@ -299,7 +299,10 @@ int prepare(sched_s* h) {
       // max blocks per SM from shared memory and registers (occupancy API)
       int bps = 0;
       const cudaError_t e = sim_occupancy(h->in.policy, 0, wpb * 32, smem, &bps, seg_cap ? 2 : ring ? 1 : 0, K);
-      if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+      if (e != cudaSuccess) {  // block larger than the kernel's launch bound: not a candidate
+        cudaGetLastError();
+        continue;
+      }
       if (bps * wpb > best_w) { best_w = bps * wpb; *wpb_out = wpb; *bps_out = bps; }
     }
     if (best_w == 0)

@@ -44,6 +44,15 @@
 #ifndef WAITSIM_WAIT_GEN_INL  // WAIT kernels inline the window generator (1) or call it (0: C2 WAIT 12.3 -> 13.5 ms)
 #define WAITSIM_WAIT_GEN_INL 1
 #endif
+#ifndef WAITSIM_WAIT2_ONEWARP  // two-class WAIT ring kernel in one-warp blocks: C2 WAIT 12.3 -> 11.4 ms
+#define WAITSIM_WAIT2_ONEWARP 1
+#endif
+#ifndef WAITSIM_WAITK_ONEWARP  // (other WAIT ring kernels one-warp: C1 / C4 within +-2%)
+#define WAITSIM_WAITK_ONEWARP 0
+#endif
+#ifndef WAITSIM_FCFS2_ONEWARP  // (FCFS in one-warp blocks: C2 FCFS 13.0 -> 13.2 ms)
+#define WAITSIM_FCFS2_ONEWARP 0
+#endif
 #ifndef WAITSIM_PEND_REDUCE_K
 #define WAITSIM_PEND_REDUCE_K 2
 #endif
@@ -2553,18 +2562,30 @@ constexpr int kMinBlocks() {
        : (POL == SCHED_FCFS && KC == 1) ? WAITSIM_MEMBER_FCFS_MINB : 2;  // one-class member FCFS (marks)
 }
 
+// one-warp blocks (the warp's shared-memory window starts at offset 0: no
+// per-warp base to rematerialise under register pressure)
+template <int POL, bool RING, int KC>
+__host__ __device__ constexpr bool kOneWarp() {
+  return RING && ((KC == 2 && POL == SCHED_WAIT && WAITSIM_WAIT2_ONEWARP) ||
+                  (KC == 2 && POL == SCHED_FCFS && WAITSIM_FCFS2_ONEWARP) ||
+                  (KC > 0 && KC != 2 && POL == SCHED_WAIT && WAITSIM_WAITK_ONEWARP));
+}
+
 template <int POL, bool TRACE, bool RING, bool SEG, int KC>
 // WAIT and the class-ring engine: <= 4 warps per block, 5 blocks per SM ->
 // <= 102 registers, 20 warps/SM (the ring engine's shared footprint is small,
 // so registers bound its occupancy: measured C2 FCFS 128 registers / 16
 // warps 20.9 ms -> 96 / 20 warps 18.7 ms; 80 / 24 warps spills, 20.7 ms);
 // the member and segment engines are shared-memory bound: 128 registers
-__global__ void __launch_bounds__((POL == SCHED_WAIT || RING) ? 128 : 256, kMinBlocks<POL, RING, KC>())
+__global__ void __launch_bounds__(kOneWarp<POL, RING, KC>() ? 32 : (POL == SCHED_WAIT || RING) ? 128 : 256,
+                                  kOneWarp<POL, RING, KC>() ? 4 * kMinBlocks<POL, RING, KC>()
+                                                            : kMinBlocks<POL, RING, KC>())
     sim_kernel(const DevParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int wib = threadIdx.x >> 5;
+  const int wib = kOneWarp<POL, RING, KC>() ? 0 : threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t slot = blockIdx.x * (blockDim.x >> 5) + (uint32_t)wib;  // SEG: global per-warp array
+  const uint32_t slot = kOneWarp<POL, RING, KC>() ? blockIdx.x
+                                                   : blockIdx.x * (blockDim.x >> 5) + (uint32_t)wib;  // SEG: global per-warp array
   WarpSim<POL, TRACE, RING, SEG, KC> sim(P, smem + (size_t)wib * P.warp_smem, lane, slot);
   for (;;) {
     uint32_t i = 0;
@@ -2599,7 +2620,11 @@ cudaError_t launch_t(const DevParams& p, int grid, int block, size_t smem, cudaS
 template <int POL, bool TRACE, bool RING = false, bool SEG = false, int KC = 0>
 cudaError_t occ_t(int block, size_t smem, int* bps) {
   auto k = sim_kernel<POL, TRACE, RING, SEG, KC>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, k);
+  if (e != cudaSuccess) return e;
+  if (block > fa.maxThreadsPerBlock) { *bps = 0; return cudaSuccess; }  // beyond the launch bound
+  e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k, block, smem);
 }
