@@ -47,6 +47,9 @@
 #ifndef WAITSIM_WAIT2_ONEWARP  // two-class WAIT ring kernel in one-warp blocks: C2 WAIT 12.3 -> 11.4 ms
 #define WAITSIM_WAIT2_ONEWARP 1
 #endif
+#ifndef WAITSIM_SEG_ONEWARP  // (segment engine one-warp: C3a 54.0 -> 58.4 ms, C3b 17.2 -> 19.1 ms: 1 KB reserved smem per block)
+#define WAITSIM_SEG_ONEWARP 0
+#endif
 #ifndef WAITSIM_WAITK_ONEWARP  // (other WAIT ring kernels one-warp: C1 / C4 within +-2%)
 #define WAITSIM_WAITK_ONEWARP 0
 #endif
@@ -2564,9 +2567,10 @@ constexpr int kMinBlocks() {
 
 // one-warp blocks (the warp's shared-memory window starts at offset 0: no
 // per-warp base to rematerialise under register pressure)
-template <int POL, bool RING, int KC>
+template <int POL, bool RING, int KC, bool SEG = false>
 __host__ __device__ constexpr bool kOneWarp() {
-  return RING && ((KC == 2 && POL == SCHED_WAIT && WAITSIM_WAIT2_ONEWARP) ||
+  return (SEG && KC > 0 && WAITSIM_SEG_ONEWARP) ||
+         RING && ((KC == 2 && POL == SCHED_WAIT && WAITSIM_WAIT2_ONEWARP) ||
                   (KC == 2 && POL == SCHED_FCFS && WAITSIM_FCFS2_ONEWARP) ||
                   (KC > 0 && KC != 2 && POL == SCHED_WAIT && WAITSIM_WAITK_ONEWARP));
 }
@@ -2577,14 +2581,14 @@ template <int POL, bool TRACE, bool RING, bool SEG, int KC>
 // so registers bound its occupancy: measured C2 FCFS 128 registers / 16
 // warps 20.9 ms -> 96 / 20 warps 18.7 ms; 80 / 24 warps spills, 20.7 ms);
 // the member and segment engines are shared-memory bound: 128 registers
-__global__ void __launch_bounds__(kOneWarp<POL, RING, KC>() ? 32 : (POL == SCHED_WAIT || RING) ? 128 : 256,
-                                  kOneWarp<POL, RING, KC>() ? 4 * kMinBlocks<POL, RING, KC>()
-                                                            : kMinBlocks<POL, RING, KC>())
+__global__ void __launch_bounds__(kOneWarp<POL, RING, KC, SEG>() ? 32 : (POL == SCHED_WAIT || RING) ? 128 : 256,
+                                  kOneWarp<POL, RING, KC, SEG>() ? (SEG ? 16 : 4 * kMinBlocks<POL, RING, KC>())
+                                                                 : kMinBlocks<POL, RING, KC>())
     sim_kernel(const DevParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int wib = kOneWarp<POL, RING, KC>() ? 0 : threadIdx.x >> 5;
+  const int wib = kOneWarp<POL, RING, KC, SEG>() ? 0 : threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t slot = kOneWarp<POL, RING, KC>() ? blockIdx.x
+  const uint32_t slot = kOneWarp<POL, RING, KC, SEG>() ? blockIdx.x
                                                    : blockIdx.x * (blockDim.x >> 5) + (uint32_t)wib;  // SEG: global per-warp array
   WarpSim<POL, TRACE, RING, SEG, KC> sim(P, smem + (size_t)wib * P.warp_smem, lane, slot);
   for (;;) {
