@@ -47,6 +47,9 @@
 #ifndef WAITSIM_WAIT2_ONEWARP  // two-class WAIT ring kernel in one-warp blocks: C2 WAIT 12.3 -> 11.4 ms
 #define WAITSIM_WAIT2_ONEWARP 1
 #endif
+#ifndef WAITSIM_FCFS4_ONEWARP  // four-class FCFS ring kernel in one-warp blocks: C3a FCFS 49.7 -> 48.3,
+#define WAITSIM_FCFS4_ONEWARP 1   // C3a_tv 46.8 -> 43.3 ms (three classes: C4 FCFS +1..3%, not used)
+#endif
 #ifndef WAITSIM_SEG_ONEWARP  // (segment engine one-warp: C3a 54.0 -> 58.4 ms, C3b 17.2 -> 19.1 ms: 1 KB reserved smem per block)
 #define WAITSIM_SEG_ONEWARP 0
 #endif
@@ -2572,7 +2575,8 @@ __host__ __device__ constexpr bool kOneWarp() {
   return (SEG && KC > 0 && WAITSIM_SEG_ONEWARP) ||
          RING && ((KC == 2 && POL == SCHED_WAIT && WAITSIM_WAIT2_ONEWARP) ||
                   (KC == 2 && POL == SCHED_FCFS && WAITSIM_FCFS2_ONEWARP) ||
-                  (KC > 0 && KC != 2 && POL == SCHED_WAIT && WAITSIM_WAITK_ONEWARP));
+                  (KC > 0 && KC != 2 && POL == SCHED_WAIT && WAITSIM_WAITK_ONEWARP) ||
+                  (KC == 4 && POL == SCHED_FCFS && WAITSIM_FCFS4_ONEWARP));
 }
 
 template <int POL, bool TRACE, bool RING, bool SEG, int KC>
