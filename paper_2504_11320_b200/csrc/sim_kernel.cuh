@@ -50,6 +50,9 @@
 #ifndef WAITSIM_FCFS4_ONEWARP  // four-class FCFS ring kernel in one-warp blocks: C3a FCFS 49.7 -> 48.3,
 #define WAITSIM_FCFS4_ONEWARP 1   // C3a_tv 46.8 -> 43.3 ms (three classes: C4 FCFS +1..3%, not used)
 #endif
+#ifndef WAITSIM_MEMBER_FCFS_ONEWARP  // (one-warp member FCFS: C3b 30.1 -> 29.5 ms, C5 FCFS 71.7 -> 74.0 ms: off)
+#define WAITSIM_MEMBER_FCFS_ONEWARP 0
+#endif
 #ifndef WAITSIM_SEG_ONEWARP  // (segment engine one-warp: C3a 54.0 -> 58.4 ms, C3b 17.2 -> 19.1 ms: 1 KB reserved smem per block)
 #define WAITSIM_SEG_ONEWARP 0
 #endif
@@ -2573,6 +2576,7 @@ constexpr int kMinBlocks() {
 template <int POL, bool RING, int KC, bool SEG = false>
 __host__ __device__ constexpr bool kOneWarp() {
   return (SEG && KC > 0 && WAITSIM_SEG_ONEWARP) ||
+         (!RING && !SEG && POL == SCHED_FCFS && KC == 1 && WAITSIM_MEMBER_FCFS_ONEWARP) ||
          RING && ((KC == 2 && POL == SCHED_WAIT && WAITSIM_WAIT2_ONEWARP) ||
                   (KC == 2 && POL == SCHED_FCFS && WAITSIM_FCFS2_ONEWARP) ||
                   (KC > 0 && KC != 2 && POL == SCHED_WAIT && WAITSIM_WAITK_ONEWARP) ||
@@ -2586,7 +2590,7 @@ template <int POL, bool TRACE, bool RING, bool SEG, int KC>
 // warps 20.9 ms -> 96 / 20 warps 18.7 ms; 80 / 24 warps spills, 20.7 ms);
 // the member and segment engines are shared-memory bound: 128 registers
 __global__ void __launch_bounds__(kOneWarp<POL, RING, KC, SEG>() ? 32 : (POL == SCHED_WAIT || RING) ? 128 : 256,
-                                  kOneWarp<POL, RING, KC, SEG>() ? (SEG ? 16 : 4 * kMinBlocks<POL, RING, KC>())
+                                  kOneWarp<POL, RING, KC, SEG>() ? (SEG ? 16 : (RING ? 4 : 8) * kMinBlocks<POL, RING, KC>())
                                                                  : kMinBlocks<POL, RING, KC>())
     sim_kernel(const DevParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
