@@ -50,6 +50,9 @@
 #ifndef WAITSIM_FCFS4_ONEWARP  // four-class FCFS ring kernel in one-warp blocks: C3a FCFS 49.7 -> 48.3,
 #define WAITSIM_FCFS4_ONEWARP 1   // C3a_tv 46.8 -> 43.3 ms (three classes: C4 FCFS +1..3%, not used)
 #endif
+#ifndef WAITSIM_FCFS1_ONEWARP  // (one-class FCFS ring one-warp: C1 FCFS 69.1 -> 71.9 ms: off)
+#define WAITSIM_FCFS1_ONEWARP 0
+#endif
 #ifndef WAITSIM_MEMBER_FCFS_ONEWARP  // (one-warp member FCFS: C3b 30.1 -> 29.5 ms, C5 FCFS 71.7 -> 74.0 ms: off)
 #define WAITSIM_MEMBER_FCFS_ONEWARP 0
 #endif
@@ -2580,7 +2583,8 @@ __host__ __device__ constexpr bool kOneWarp() {
          RING && ((KC == 2 && POL == SCHED_WAIT && WAITSIM_WAIT2_ONEWARP) ||
                   (KC == 2 && POL == SCHED_FCFS && WAITSIM_FCFS2_ONEWARP) ||
                   (KC > 0 && KC != 2 && POL == SCHED_WAIT && WAITSIM_WAITK_ONEWARP) ||
-                  (KC == 4 && POL == SCHED_FCFS && WAITSIM_FCFS4_ONEWARP));
+                  (KC == 4 && POL == SCHED_FCFS && WAITSIM_FCFS4_ONEWARP) ||
+                  (KC == 1 && POL == SCHED_FCFS && WAITSIM_FCFS1_ONEWARP));
 }
 
 template <int POL, bool TRACE, bool RING, bool SEG, int KC>
