@@ -68,7 +68,7 @@
 #ifndef WAITSIM_PEND_REDUCE_K
 #define WAITSIM_PEND_REDUCE_K 2
 #endif
-#ifndef WAITSIM_WAIT2_MINB  // two-class WAIT ring kernel: 6 (80 registers); 5: 13.7 ms, 7: 14.2 ms vs 13.0
+#ifndef WAITSIM_WAIT2_MINB  // two-class WAIT ring kernel: 6 (80 registers); 4-warp blocks 5 / 7: 13.7 / 14.2 vs 13.0 ms; one-warp 5 / 7: 12.2 / 11.7 vs 11.4 ms
 #define WAITSIM_WAIT2_MINB 6
 #endif
 #ifndef WAITSIM_MEMBER_FCFS_MINB  // member-engine FCFS (length marks), blocks of 8 warps: 3 (80
